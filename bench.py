@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark: MG-Tree temporal motif co-mining on B200 (one JSON line on rank 0).
+
+A step = one co-mining query of the configured motif group over ALL root edges of
+the workload graph (window-end kernel + co-mining kernel on every rank, over a
+work-balanced timestamp-range split of the roots, then one NCCL all-reduce of
+the per-motif u64 counts when N > 1).  Inputs are resident in HBM; L2 (126 MB)
+is flushed by a 512 MiB write between timed steps; per-step device time comes
+from CUDA events on the launching stream; the job time is the max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl mayura|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Also reported: e2e (the public C-ABI path from host edge arrays: host build +
+H2D + kernels + D2H of the counts), the independent per-motif GPU baseline (same
+kernel, one single-motif tree per motif), roofline (algorithmic bytes of the
+co-mining kernel / its event-timed duration vs measured HBM copy bandwidth),
+clocks sampled during the timed region, and the CPU oracle timed on host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "motif-group co-mining time (s) and root edges/s at 1/2/4/8 B200; HBM GB/s frac"
+UNIT = "root edges/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["mayura", "reference"], default="mayura")
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--flush-mb", type=int, default=512)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-indep", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--profile", action="store_true", help="short run for ncu: no extras")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(1)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 10:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[6:10]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ oracle (CPU) --
+def cpu_baseline(cfg, src, dst, t, V, budget_s: float):
+    """The oracle as it stands (O2, per-motif Algorithm 1, all host cores), timed on a
+    bounded sample of the workload: the full root range if one pass fits the budget,
+    else a contiguous root range scaled to ~budget_s.  Returns (record, counts or None)."""
+    import oracle
+    threads = os.cpu_count() or 1
+    E = len(src)
+    probe = min(E, 20_000)
+    a = max(0, E // 2 - probe // 2)
+    t0 = time.perf_counter()
+    oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=(a, a + probe), threads=threads)
+    per_root = (time.perf_counter() - t0) / max(probe, 1)
+    if per_root * E <= budget_s:
+        rng, sample = (0, E), "full workload (all %d roots, all %d motifs, mined independently)" % (E, len(cfg.motifs))
+    else:
+        n = max(1000, int(budget_s / max(per_root, 1e-12)))
+        a = max(0, E // 2 - n // 2)
+        rng = (a, min(E, a + n))
+        sample = "contiguous root range [%d, %d) of %d (%.1f%%), all %d motifs" % (
+            rng[0], rng[1], E, 100.0 * (rng[1] - rng[0]) / E, len(cfg.motifs))
+    reps, elapsed, counts = 0, 0.0, None
+    while reps < 1 or (elapsed < 3.0 and reps < 5):
+        t0 = time.perf_counter()
+        counts = oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=rng, threads=threads)
+        elapsed += time.perf_counter() - t0
+        reps += 1
+    roots = (rng[1] - rng[0]) * reps
+    rec = {"value": roots / elapsed, "unit": UNIT, "cores": threads, "kind": "oracle",
+           "sample": sample + ("; %d passes" % reps), "seconds": elapsed / reps}
+    return rec, (counts if rng == (0, E) else None), rng
+
+
+def config_record(cfg, world, flush_mb):
+    return {"workload": "%s: %s" % (cfg.name, cfg.title), "name": cfg.name, "n_vertices": cfg.n_vertices,
+            "n_edges": cfg.n_edges, "delta": cfg.delta, "motifs": list(cfg.motifs),
+            "generator": "cascade-Zipf alpha=%g p=%g tau=%gs span=%ds seed=%d" % (
+                cfg.alpha, cfg.p, cfg.tau, cfg.span, cfg.seed),
+            "parallelism": "root-partition%d" % world,
+            "l2": "flushed between timed steps (%d MiB write)" % flush_mb}
+
+
+def run_reference(args, cfg, world, rank):
+    """--impl reference: the CPU oracle (the only reference this paper-only tier has)."""
+    if rank != 0:
+        return
+    src, dst, t, V = cfg.graph()
+    import oracle
+    oracle.build()
+    threads = os.cpu_count() or 1
+    E = len(src)
+    probe = min(E, 20_000)
+    a = max(0, E // 2 - probe // 2)
+    t0 = time.perf_counter()
+    oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=(a, a + probe), threads=threads)
+    per_root = (time.perf_counter() - t0) / max(probe, 1)
+    step_budget = max(1.0, 150.0 / max(1, args.steps + args.warmup))
+    n = E if per_root * E <= step_budget else max(1000, int(step_budget / max(per_root, 1e-12)))
+    a = max(0, E // 2 - n // 2)
+    rng = (a, min(E, a + n))
+    for _ in range(args.warmup):
+        oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=rng, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=rng, threads=threads)
+    el = time.perf_counter() - t0
+    value = (rng[1] - rng[0]) * args.steps / el
+    sample = ("full workload" if rng == (0, E) else "root range [%d, %d) of %d" % (rng[0], rng[1], E))
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+           "data": "synthetic", "config": config_record(cfg, 1, 0),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                            "sample": sample + " per step; O2 per-motif Algorithm-1 backtracking"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    assert torch.cuda.is_available(), "bench.py needs a GPU"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import __graft_entry__
+    if rank == 0 and __graft_entry__._builder()._stale():
+        __graft_entry__._builder().build()
+    if world > 1:
+        dist.barrier()
+    import paper_2507_14813_b200 as M
+
+    src, dst, t, V = cfg.graph()
+    E = len(src)
+    g = M.Graph(src, dst, t, V, device=local)
+    tree = M.MGTree(cfg.group(), cfg.delta)
+    k = tree.n_motifs
+    bounds = g.partition(cfg.delta, world)
+    rb, re_ = bounds[rank], bounds[rank + 1]
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    counts = torch.zeros(k, dtype=torch.int64, device=dev)
+    flush = torch.empty(args.flush_mb * (1 << 20) // 4, dtype=torch.int32, device=dev)
+
+    def make_events(n):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+        for e in evs:
+            e.record(stream)  # materialise the cudaEvent_t before handing it to the library
+        return evs
+
+    def timed(independent: bool, steps: int, warmup: int):
+        ev = [make_events(4) for _ in range(steps)]
+        for i in range(warmup):
+            flush.fill_(i)
+            M.mayura_comine_ex(g.handle, tree.handle, rb, re_, sp, counts, independent, ev[0][1].cuda_event)
+            if world > 1:
+                dist.all_reduce(counts)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(steps):
+            flush.fill_(i + 1)                              # evict L2 outside the step's events
+            e0, em, ek, e1 = ev[i]
+            e0.record(stream)
+            M.mayura_comine_ex(g.handle, tree.handle, rb, re_, sp, counts, independent, em.cuda_event)
+            ek.record(stream)
+            if world > 1:
+                dist.all_reduce(counts)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        step_ms = sum(e0.elapsed_time(e1) for e0, _, _, e1 in ev)
+        kern_ms = sum(em.elapsed_time(ek) for _, em, ek, _ in ev)
+        win_ms = sum(e0.elapsed_time(em) for e0, em, _, _ in ev)
+        tt = torch.tensor([step_ms, kern_ms, win_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return [x / steps for x in tt.tolist()], counts.cpu().tolist()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    (ms_step, ms_kern, ms_win), got = timed(False, args.steps, args.warmup)
+    clocks = sampler.stop()
+
+    indep = None
+    if not args.no_indep and not args.profile:
+        (ims_step, ims_kern, _), igot = timed(True, max(3, args.steps // 2), 2)
+        indep = {"ms_per_step": ims_step, "kernel_ms": ims_kern, "speedup_comine": ims_step / ms_step,
+                 "counts_equal": igot == got,
+                 "paper_context": "paper avg co-mining speedup 1.7x GPU (A40) / 2.4x CPU (Xeon 8380), PAPER.md:41"}
+
+    # algorithmic bytes of the co-mining kernel for this rank's range (instrumented run, untimed)
+    st = M.mayura_comine_stats(g.handle, tree.handle, rb, re_, False)
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(peaks_path):
+        peak, peak_src = json.load(open(peaks_path))["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs (measured)"
+    else:
+        peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    achieved = st["bytes_alg"] / (ms_kern * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        tr = json.load(open(prof)).get(cfg.name)
+        if tr:
+            traffic = tr.get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "comine_kernel", "kernel_ms": ms_kern,
+                "window_end_kernel_ms": ms_win, "bytes_alg_per_launch": st["bytes_alg"],
+                "bytes_alg_per_root": st["bytes_alg"] / max(1, re_ - rb), "peak_source": peak_src,
+                "note": "latency-bound irregular traversal; frac = algorithmic bytes / event-timed duration"}
+
+    # e2e through the public C ABI from host buffers
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        pin_src = torch.from_numpy(src).pin_memory().numpy()
+        pin_dst = torch.from_numpy(dst).pin_memory().numpy()
+        pin_t = torch.from_numpy(t).pin_memory().numpy()
+        tsteps = []
+        for i in range(args.e2e_steps + 1):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            g2 = M.Graph(pin_src, pin_dst, pin_t, V, device=local)   # host build + H2D
+            if world > 1:
+                b2 = g2.partition(cfg.delta, world)
+                c2 = torch.zeros(k, dtype=torch.int64, device=dev)
+                M.mayura_comine(g2.handle, tree.handle, b2[rank], b2[rank + 1], sp, c2)
+                dist.all_reduce(c2)
+                host_counts = c2.cpu().tolist()                          # D2H
+            else:
+                host_counts = M.comine(g2, tree)                         # kernels + D2H
+            g2.close()
+            el = time.perf_counter() - t0
+            if i > 0:
+                tsteps.append(el)
+            assert host_counts == got
+        tt = torch.tensor([statistics.mean(tsteps)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": E / tt.item(), "unit": UNIT, "s_per_step": tt.item(),
+               "h2d_bytes_per_step": 36 * E + 8 * (V + 1), "d2h_bytes_per_step": 8 * k,
+               "path": "mayura_load_graph(host arrays: sort+CSR on host, H2D) + mayura_comine + D2H counts"}
+
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        cpu, ocounts, orng = cpu_baseline(cfg, src, dst, t, V, args.cpu_budget_s)
+        if ocounts is not None:
+            parity = "exact" if ocounts == got else "MISMATCH"
+        else:
+            sub = torch.zeros(k, dtype=torch.int64, device=dev)
+            import oracle
+            ocounts = oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=orng)
+            M.mayura_comine(g.handle, tree.handle, orng[0], orng[1], sp, sub)
+            parity = "exact on sampled root range" if sub.cpu().tolist() == ocounts else "MISMATCH"
+
+    if rank == 0:
+        launches_per_rank = args.steps * 2
+        out = {"metric": METRIC, "value": E / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+               "data": "synthetic", "config": config_record(cfg, world, args.flush_mb),
+               "co_mining_time_s": ms_step * 1e-3, "counts": dict(zip(cfg.motifs, got)),
+               "parity_vs_oracle": parity,
+               "gpu_launches": launches_per_rank * world,
+               "gpu_launches_detail": "per rank per step: window_end_kernel + comine_kernel",
+               "roofline": roofline, "clocks": clocks, "e2e": e2e, "independent_gpu": indep,
+               "cpu_baseline": cpu, "search_stats": st}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,135 @@
+// capi.cpp -- host-only entry points of the C ABI (include/mayura.h): errors,
+// graph inspection, MG-Tree build/inspection, multi-GPU root partitioning.
+#include <algorithm>
+#include <cstring>
+#include <new>
+
+#include "internal.h"
+
+namespace mayura {
+static thread_local std::string g_last_error;
+
+mayura_status fail(mayura_status s, const std::string &msg) {
+    g_last_error = msg;
+    return s;
+}
+void clear_error() { g_last_error.clear(); }
+}  // namespace mayura
+
+using namespace mayura;
+
+extern "C" const char *mayura_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" const char *mayura_version(void) { return "mayura-b200 0.1 sm_100a"; }
+
+extern "C" mayura_status mayura_graph_info(mayura_graph g, uint64_t *n_edges, uint32_t *n_vertices,
+                                           uint64_t *device_bytes) {
+    clear_error();
+    if (!g) return fail(MAYURA_E_INVALID, "mayura_graph_info: NULL handle");
+    if (n_edges) *n_edges = g->E;
+    if (n_vertices) *n_vertices = g->V;
+    if (device_bytes) *device_bytes = g->device_bytes;
+    return MAYURA_OK;
+}
+
+extern "C" mayura_status mayura_graph_export(mayura_graph g, uint32_t *src, uint32_t *dst, int64_t *t,
+                                             uint32_t *tr, uint64_t *perm, uint32_t *out_off,
+                                             uint32_t *out_ent, uint32_t *in_off, uint32_t *in_ent) {
+    clear_error();
+    if (!g) return fail(MAYURA_E_INVALID, "mayura_graph_export: NULL handle");
+    const size_t E = (size_t)g->E, V1 = (size_t)g->V + 1;
+    if (src) std::memcpy(src, g->src.data(), 4 * E);
+    if (dst) std::memcpy(dst, g->dst.data(), 4 * E);
+    if (t) std::memcpy(t, g->t.data(), 8 * E);
+    if (tr) std::memcpy(tr, g->tr.data(), 4 * E);
+    if (perm) std::memcpy(perm, g->perm.data(), 8 * E);
+    if (out_off) std::memcpy(out_off, g->out_off.data(), 4 * V1);
+    if (in_off) std::memcpy(in_off, g->in_off.data(), 4 * V1);
+    if (out_ent) std::memcpy(out_ent, g->out_ent.data(), 8 * E);
+    if (in_ent) std::memcpy(in_ent, g->in_ent.data(), 8 * E);
+    return MAYURA_OK;
+}
+
+extern "C" mayura_status mayura_build_mgtree(const uint32_t *motif_edges, const uint32_t *motif_len,
+                                             uint32_t n_motifs, int64_t delta, mayura_mgtree *out) {
+    clear_error();
+    if (!out) return fail(MAYURA_E_INVALID, "mayura_build_mgtree: out is NULL");
+    mayura_mgtree_s *m = new (std::nothrow) mayura_mgtree_s();
+    if (!m) return fail(MAYURA_E_OOM, "mayura_build_mgtree: out of host memory");
+    mayura_status s;
+    try {
+        s = compile_tree(motif_edges, motif_len, n_motifs, delta, m);
+    } catch (const std::bad_alloc &) {
+        s = fail(MAYURA_E_OOM, "mayura_build_mgtree: out of host memory");
+    }
+    if (s != MAYURA_OK) {
+        delete m;
+        return s;
+    }
+    *out = m;
+    return MAYURA_OK;
+}
+
+extern "C" mayura_status mayura_mgtree_info(mayura_mgtree m, uint32_t *n_motifs, uint32_t *n_trie_nodes,
+                                            uint32_t *n_mg_nodes, uint32_t *max_vertices, uint32_t *max_edges,
+                                            double *sm) {
+    clear_error();
+    if (!m) return fail(MAYURA_E_INVALID, "mayura_mgtree_info: NULL handle");
+    if (n_motifs) *n_motifs = m->n_motifs;
+    if (n_trie_nodes) *n_trie_nodes = (uint32_t)m->group.nodes.size();
+    if (n_mg_nodes) *n_mg_nodes = m->n_mg_nodes;
+    if (max_vertices) *max_vertices = m->group.max_vertices;
+    if (max_edges) *max_edges = m->group.max_edges;
+    if (sm) *sm = m->sm;
+    return MAYURA_OK;
+}
+
+extern "C" mayura_status mayura_mgtree_dump(mayura_mgtree m, char *buf, size_t cap, size_t *needed) {
+    clear_error();
+    if (!m) return fail(MAYURA_E_INVALID, "mayura_mgtree_dump: NULL handle");
+    if (needed) *needed = m->dump.size() + 1;
+    if (buf && cap > 0) {
+        size_t n = std::min(cap - 1, m->dump.size());
+        std::memcpy(buf, m->dump.data(), n);
+        buf[n] = 0;
+    }
+    return MAYURA_OK;
+}
+
+extern "C" void mayura_free_mgtree(mayura_mgtree m) {
+    if (!m) return;
+    free_mgtree_device(m);
+    delete m;
+}
+
+// Work-balanced contiguous split of the root ids: proxy work of root r
+// = 1 + |{e : t_r < t_e <= t_r + delta}|, computed with two pointers over the
+// time-sorted timestamps; cut points at equal shares of the prefix sum.
+extern "C" mayura_status mayura_partition_roots(mayura_graph g, int64_t delta, uint32_t n_parts,
+                                                uint64_t *bounds_out) {
+    clear_error();
+    if (!g || !bounds_out || n_parts == 0) return fail(MAYURA_E_INVALID, "mayura_partition_roots: bad argument");
+    if (delta < 0) return fail(MAYURA_E_INVALID, "mayura_partition_roots: delta < 0");
+    const uint64_t E = g->E;
+    const std::vector<int64_t> &t = g->t;
+    std::vector<uint64_t> pref(E + 1, 0);
+    uint64_t j = 0, k = 0;  // j: first index with t > t_r ; k: first index with t > t_r + delta
+    for (uint64_t r = 0; r < E; r++) {
+        const int64_t lim = (delta > INT64_MAX - t[r]) ? INT64_MAX : t[r] + delta;
+        if (j < r + 1) j = r + 1;
+        while (j < E && t[j] <= t[r]) j++;
+        if (k < j) k = j;
+        while (k < E && t[k] <= lim) k++;
+        pref[r + 1] = pref[r] + 1 + (k - j);
+    }
+    const uint64_t total = pref[E];
+    bounds_out[0] = 0;
+    for (uint32_t p = 1; p < n_parts; p++) {
+        const long double target = (long double)total * p / n_parts;
+        uint64_t b = (uint64_t)(std::lower_bound(pref.begin(), pref.end(), (uint64_t)target) - pref.begin());
+        b = std::min<uint64_t>(b, E);
+        bounds_out[p] = std::max(b, bounds_out[p - 1]);
+    }
+    bounds_out[n_parts] = E;
+    return MAYURA_OK;
+}

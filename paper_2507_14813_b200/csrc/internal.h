@@ -1,0 +1,99 @@
+// internal.h -- shared host/device declarations of libmayura (not part of the ABI).
+#pragma once
+
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/mayura.h"
+
+namespace mayura {
+
+// ------------------------------------------------------------------ errors --
+mayura_status fail(mayura_status s, const std::string &msg);
+void clear_error();
+
+// ------------------------------------------------------------ device table --
+// One row per trie node = one distinct canonical edge prefix.
+// Rows are laid out in BFS order with the children of every node contiguous and
+// grouped by anchor, so a group is a contiguous child range.
+enum AnchorKind : uint8_t { ANCHOR_OUT = 0, ANCHOR_IN = 1, ANCHOR_GLOBAL = 2 };
+static constexpr uint8_t CLS_NEW = 0xFF;  // "graph vertex not yet in the image of m2g"
+
+struct DNode {             // 8 bytes
+    uint8_t want;          // OUT child: mapped motif vertex the dst must equal, or CLS_NEW
+    uint8_t n_new;         // motif vertices this node's edge maps for the first time (0,1,2)
+    uint8_t nv;            // mapped motif vertices after this node's edge
+    uint8_t flags;         // bit0: completion (some motif == this prefix), bit1: has children
+    uint16_t group_begin;  // groups of this node's children
+    uint16_t group_end;
+};
+struct DGroup {            // 8 bytes
+    uint8_t kind;          // AnchorKind
+    uint8_t anchor;        // motif vertex whose adjacency is scanned (OUT: u, IN: v)
+    uint8_t n_inner;       // children that have children themselves
+    uint8_t pad;
+    uint16_t child_begin;  // contiguous node rows
+    uint16_t child_end;
+};
+static constexpr uint8_t NODE_COMPLETION = 1, NODE_INNER = 2;
+
+struct Table {
+    std::vector<DNode> nodes;          // row 0 = root (canonical edge 0->1)
+    std::vector<DGroup> groups;
+    std::vector<uint32_t> motif_node;  // per input motif: its row
+    uint32_t max_vertices = 2, max_edges = 1;
+};
+
+}  // namespace mayura
+
+// ------------------------------------------------------------------ handles --
+struct mayura_graph_s {
+    uint64_t E = 0;
+    uint32_t V = 0;
+    int device = -1;
+    // host build results (edge id order)
+    std::vector<uint32_t> src, dst, tr;
+    std::vector<int64_t> t;
+    std::vector<uint64_t> perm;
+    std::vector<uint32_t> out_off, in_off;  // V+1
+    std::vector<uint32_t> out_ent, in_ent;  // 2E: (tr, nbr)
+    // device arrays
+    uint32_t *d_src = nullptr, *d_dst = nullptr, *d_tr = nullptr, *d_hi = nullptr;
+    int64_t *d_t = nullptr;
+    uint32_t *d_out_off = nullptr, *d_in_off = nullptr;
+    uint32_t *d_out_ent = nullptr, *d_in_ent = nullptr;  // uint2 {tr, nbr}
+    uint32_t *d_queue = nullptr;                         // work-queue cursors
+    unsigned long long *d_counts = nullptr;              // scratch counts (host-output calls)
+    uint32_t d_counts_cap = 0;
+    unsigned long long *d_stats = nullptr;
+    uint64_t device_bytes = 0;
+};
+
+struct mayura_mgtree_s {
+    int64_t delta = 0;
+    uint32_t n_motifs = 0;
+    std::vector<std::vector<std::pair<uint32_t, uint32_t>>> canon;  // canonical motifs
+    mayura::Table group;                  // co-mining table
+    std::vector<mayura::Table> single;    // one single-motif table per motif
+    // path-compressed MG-Tree view
+    uint32_t n_mg_nodes = 0;
+    double sm = 0.0;
+    std::string dump;
+    // lazily uploaded device copies: [0] = group, [1..k] = singles
+    int dev = -1;
+    std::vector<void *> d_tables;
+};
+
+namespace mayura {
+mayura_status build_graph_host(const uint32_t *src, const uint32_t *dst, const int64_t *t,
+                               uint64_t E, uint32_t V, mayura_graph_s *g);
+mayura_status compile_tree(const uint32_t *motif_edges, const uint32_t *motif_len,
+                           uint32_t n_motifs, int64_t delta, mayura_mgtree_s *m);
+int host_threads();
+}  // namespace mayura
+
+namespace mayura {
+void free_mgtree_device(mayura_mgtree_s *m);
+}

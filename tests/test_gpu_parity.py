@@ -1,0 +1,191 @@
+"""GPU parity: the CUDA co-mining path (through the C ABI) vs the CPU oracle, bit-exact.
+
+Integer counts -> the bar is exact equality.  Covered: hand-worked
+examples, >= 200 random groups of 2-6 motifs on tie-heavy fuzz graphs,
+closed forms at 10^5-10^6 edges, the full 3-edge family (87 motifs; every anchor kind
+including the all-edges candidate path), the C1/C2/C3 workloads in full, sampled
+root ranges, co-mined == independent, range additivity, edge cases."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from tests import _pins
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "hand_examples.json")
+
+
+@pytest.fixture(scope="module")
+def M():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2507_14813_b200 as M
+    return M
+
+
+def gpu_counts(M, src, dst, t, V, motifs, delta, root_range=None, independent=False):
+    g = M.Graph(src, dst, t, V, device=0)
+    tree = M.MGTree(motifs, delta)
+    fn = M.mine_independent if independent else M.comine
+    out = fn(g, tree, root_range)
+    g.close()
+    tree.close()
+    return out
+
+
+def test_hand_examples(M):
+    cases = json.load(open(GOLDEN))["cases"]
+    for c in cases:
+        e = np.array(c["edges"], dtype=np.int64).reshape(-1, 3)
+        V = int(e[:, :2].max()) + 1
+        got = gpu_counts(M, e[:, 0], e[:, 1], e[:, 2], V, [[tuple(x) for x in c["motif"]]], c["delta"])
+        assert got == [c["expected"]], c["name"]
+
+
+def test_fuzz_groups_vs_oracle(M, oracle_mod):
+    """>= 200 random groups of 2-6 motifs (<= 4 edges, some prefix-disconnected) on
+    random tie-heavy multigraphs with self-loops."""
+    nz = 0
+    for seed in range(220):
+        rng = np.random.default_rng(seed)
+        V = int(rng.integers(3, 30))
+        E = int(rng.integers(1, 300))
+        src, dst, t, V = synth.random_graph(seed, V, E, int(rng.integers(5, 200)))
+        k = int(rng.integers(2, 7))
+        motifs = [synth.random_motif(seed * 101 + j, int(rng.integers(1, 5)), int(rng.integers(2, 6)))
+                  for j in range(k)]
+        delta = int(rng.integers(0, 80))
+        exp = oracle_mod.backtrack(src, dst, t, V, motifs, delta)
+        got = gpu_counts(M, src, dst, t, V, motifs, delta)
+        assert got == exp, (seed, motifs, delta)
+        ind = gpu_counts(M, src, dst, t, V, motifs, delta, independent=True)
+        assert ind == exp, (seed, motifs, delta)
+        nz += sum(1 for x in exp if x)
+    assert nz > 300
+
+
+def test_hub_lists_longer_than_a_warp(M, oracle_mod):
+    """Few vertices, many edges: adjacency lists of 10^3-10^4 entries exercise the
+    32-ary window search and multi-batch windows."""
+    for seed in range(6):
+        src, dst, t, V = synth.random_graph(70 + seed, 5 + seed, 20_000, 4_000 + 3000 * seed, 0.01)
+        motifs = synth.group(synth.GROUP_C2) + [synth.MOTIFS["recip2"], synth.MOTIFS["repeat2"]]
+        delta = 10 + 7 * seed
+        assert gpu_counts(M, src, dst, t, V, motifs, delta) == \
+            oracle_mod.backtrack(src, dst, t, V, motifs, delta)
+
+
+def test_closed_forms_at_scale(M):
+    n = 200_000
+    src, dst, t, V = synth.out_star(n)
+    got = gpu_counts(M, src, dst, t, V, [synth.MOTIFS["star_out3"], synth.MOTIFS["star_out4"],
+                                         synth.MOTIFS["edge1"]], 40)
+    assert got == [_pins.star_fanout_count(n, 3, 40), _pins.star_fanout_count(n, 4, 40), n]
+    n = 1_000_001
+    src, dst, t, V = synth.alternating_pair(n)
+    got = gpu_counts(M, src, dst, t, V, [synth.MOTIFS["recip2"], synth.MOTIFS["repeat2"],
+                                         synth.MOTIFS["pingpong3"]], 9)
+    assert got == [_pins.alt_reciprocal(n, 9), _pins.alt_repeat(n, 9), _pins.alt_pingpong(n, 9)]
+    L, n = 4, 400_000
+    src, dst, t, V = synth.cycle_graph(L, n)
+    cyc = [(i, (i + 1) % L) for i in range(L)]
+    got = gpu_counts(M, src, dst, t, V, [cyc, [(0, 1), (1, 2), (2, 3)]], 23)
+    assert got == [_pins.cycle_graph_path(L, n, L, 23), _pins.cycle_graph_path(L, n, 3, 23)]
+
+
+@pytest.mark.parametrize("m", [2, 3])
+def test_full_family_identity(M, m):
+    fam = _pins.canonical_motifs(m)
+    for seed in range(3):
+        src, dst, t, V = synth.random_graph(600 + seed, 9, 400, 300, self_loop_frac=0.05)
+        got = gpu_counts(M, src, dst, t, V, fam, 25)
+        assert sum(got) == _pins.family_total(src, dst, t, m, 25)
+
+
+def test_full_family_vs_oracle(M, oracle_mod):
+    fam = _pins.canonical_motifs(3)
+    src, dst, t, V = synth.random_graph(4321, 7, 300, 120, self_loop_frac=0.05)
+    assert gpu_counts(M, src, dst, t, V, fam, 15) == oracle_mod.backtrack(src, dst, t, V, fam, 15)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_config_full_parity(M, oracle_mod, name):
+    cfg = synth.CONFIGS[name]
+    src, dst, t, V = cfg.graph()
+    exp = oracle_mod.backtrack(src, dst, t, V, cfg.group(), cfg.delta)
+    assert gpu_counts(M, src, dst, t, V, cfg.group(), cfg.delta) == exp
+    assert gpu_counts(M, src, dst, t, V, cfg.group(), cfg.delta, independent=True) == exp
+
+
+@pytest.mark.slow
+def test_config_c3_full_parity(M, oracle_mod):
+    cfg = synth.CONFIGS["C3"]
+    src, dst, t, V = cfg.graph()
+    exp = oracle_mod.backtrack(src, dst, t, V, cfg.group(), cfg.delta)
+    assert gpu_counts(M, src, dst, t, V, cfg.group(), cfg.delta) == exp
+
+
+def test_range_additivity_and_sampled_ranges(M, oracle_mod):
+    cfg = synth.CONFIGS["C2"]
+    src, dst, t, V = cfg.graph()
+    g = M.Graph(src, dst, t, V, device=0)
+    tree = M.MGTree(cfg.group(), cfg.delta)
+    full = M.comine(g, tree)
+    cuts = [0, 1, 31, 33, 100_000, 250_007, g.n_edges]
+    parts = [M.comine(g, tree, (a, b)) for a, b in zip(cuts[:-1], cuts[1:])]
+    assert [sum(x) for x in zip(*parts)] == full
+    for a, b in [(0, 4096), (165_000, 169_096), (g.n_edges - 4096, g.n_edges)]:
+        assert M.comine(g, tree, (a, b)) == oracle_mod.backtrack(src, dst, t, V, cfg.group(), cfg.delta,
+                                                                 root_range=(a, b))
+    assert M.comine(g, tree, (5, 5)) == [0] * tree.n_motifs
+
+
+def test_edge_cases(M, oracle_mod):
+    tri = [synth.MOTIFS["tri_cycle"], synth.MOTIFS["edge1"]]
+    assert gpu_counts(M, [], [], [], 3, tri, 10) == [0, 0]                 # empty graph
+    assert gpu_counts(M, [1, 2, 2], [1, 2, 2], [1, 2, 3], 3, tri, 10) == [0, 0]   # all self-loops
+    s, d, t = [0, 1, 2], [1, 2, 0], [5, 5, 5]
+    assert gpu_counts(M, s, d, t, 3, tri, 100) == [0, 3]                    # all tied
+    src, dst, t, V = synth.random_graph(9, 10, 500, 100)
+    assert gpu_counts(M, src, dst, t, V, synth.group(synth.GROUP_C2), 0) == \
+        oracle_mod.backtrack(src, dst, t, V, synth.group(synth.GROUP_C2), 0)   # delta = 0
+    big = 2 ** 62
+    assert gpu_counts(M, [0, 1], [1, 0], [big, big + 5], 2, [synth.MOTIFS["recip2"]], 2 ** 62) == [1]
+
+
+def test_disconnected_prefix_motifs(M, oracle_mod):
+    """(0->1, 2->3, ...) motifs use the all-edges (GLOBAL) candidate path (reading R6)."""
+    motifs = [[(0, 1), (2, 3)], [(0, 1), (2, 3), (3, 0)], [(0, 1), (2, 3), (1, 2)], [(0, 1), (2, 3), (4, 5)]]
+    for seed in range(5):
+        src, dst, t, V = synth.random_graph(50 + seed, 12, 250, 150)
+        assert gpu_counts(M, src, dst, t, V, motifs, 20) == oracle_mod.backtrack(src, dst, t, V, motifs, 20)
+
+
+def test_counts_on_device_and_stream(M, oracle_mod):
+    import torch
+    cfg = synth.CONFIGS["C1"]
+    src, dst, t, V = cfg.graph()
+    g = M.Graph(src, dst, t, V, device=0)
+    tree = M.MGTree(cfg.group(), cfg.delta)
+    out = torch.full((tree.n_motifs,), -1, dtype=torch.int64, device="cuda:0")
+    s = torch.cuda.Stream()
+    M.comine(g, tree, None, stream=s.cuda_stream, counts_out=out)
+    s.synchronize()
+    assert out.cpu().tolist() == oracle_mod.backtrack(src, dst, t, V, cfg.group(), cfg.delta)
+
+
+def test_stats_kernel_counts_and_work(M):
+    cfg = synth.CONFIGS["C1"]
+    src, dst, t, V = cfg.graph()
+    g = M.Graph(src, dst, t, V, device=0)
+    tree = M.MGTree(cfg.group(), cfg.delta)
+    st = M.comine_stats(g, tree)
+    si = M.comine_stats(g, tree, independent=True)
+    assert st["matches"] == sum(M.comine(g, tree))
+    assert st["roots"] == int((src != dst).sum())
+    assert st["entries"] < si["entries"] and st["bytes_alg"] < si["bytes_alg"]  # co-mining removes work

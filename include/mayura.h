@@ -86,12 +86,19 @@ mayura_status mayura_graph_info(mayura_graph g, uint64_t *n_edges, uint32_t *n_v
  *   src,dst,tr [E] u32 / t [E] i64 : edges in id order; tr[e] = id of the first
  *                                    edge with timestamp t[e] (time rank);
  *   perm [E] u64                   : input rank of edge id e;
- *   out_off,in_off [V+1] u32       : CSR offsets;
- *   out_ent,in_ent [2E] u32        : CSR entries (tr, neighbour) pairs, each list in
+ *   out_off,in_off [V+1] u32       : CSR offsets; the list of vertex x occupies
+ *                                    [off[x], off[x+1]-1) and is followed by one sentinel
+ *                                    entry (0xFFFFFFFF, 0xFFFFFFFF) at off[x+1]-1;
+ *   out_ent,in_ent [2(E+V)] u32    : CSR entries (tr, neighbour) pairs, each list in
  *                                    increasing edge id (= timestamp) order. */
 mayura_status mayura_graph_export(mayura_graph g, uint32_t *src, uint32_t *dst, int64_t *t,
                                   uint32_t *tr, uint64_t *perm, uint32_t *out_off,
                                   uint32_t *out_ent, uint32_t *in_off, uint32_t *in_ent);
+
+/* Successor pointers of every edge, eptr [4E] u32: for edge e = (a, b),
+ * eptr[4e+0..3] = first position (in out_ent / in_ent entry units) with time rank > tr[e]
+ * in out(a), in(b), out(b), in(a) respectively (the sentinel position if none). */
+mayura_status mayura_graph_export_succ(mayura_graph g, uint32_t *eptr);
 
 void mayura_free_graph(mayura_graph g);
 
@@ -171,7 +178,9 @@ mayura_status mayura_comine_ex(mayura_graph g, mayura_mgtree m, uint64_t root_be
  * stats_out[0..7] = roots visited (non-self-loop), search-tree nodes expanded (partial
  * matches whose children were examined), windows located, window entries examined,
  * search probes (32-ary sample loads), batches loaded, algorithmic bytes B_alg
- * (DESIGN.md §6), matches counted.  Host output; synchronises. */
+ * (DESIGN.md §6), matches counted; stats_out[8..9] = load-balance offloads (a warp
+ * split the rest of a long window into queued contexts), contexts processed.
+ * stats_out must hold 10 entries.  Host output; synchronises. */
 mayura_status mayura_comine_stats(mayura_graph g, mayura_mgtree m, uint64_t root_begin,
                                   uint64_t root_end, int independent, uint64_t *stats_out);
 

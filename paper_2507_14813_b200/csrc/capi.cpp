@@ -45,8 +45,15 @@ extern "C" mayura_status mayura_graph_export(mayura_graph g, uint32_t *src, uint
     if (perm) std::memcpy(perm, g->perm.data(), 8 * E);
     if (out_off) std::memcpy(out_off, g->out_off.data(), 4 * V1);
     if (in_off) std::memcpy(in_off, g->in_off.data(), 4 * V1);
-    if (out_ent) std::memcpy(out_ent, g->out_ent.data(), 8 * E);
-    if (in_ent) std::memcpy(in_ent, g->in_ent.data(), 8 * E);
+    if (out_ent) std::memcpy(out_ent, g->out_ent.data(), 4 * g->out_ent.size());
+    if (in_ent) std::memcpy(in_ent, g->in_ent.data(), 4 * g->in_ent.size());
+    return MAYURA_OK;
+}
+
+extern "C" mayura_status mayura_graph_export_succ(mayura_graph g, uint32_t *eptr) {
+    clear_error();
+    if (!g || !eptr) return fail(MAYURA_E_INVALID, "mayura_graph_export_succ: NULL argument");
+    std::memcpy(eptr, g->eptr.data(), 4 * g->eptr.size());
     return MAYURA_OK;
 }
 

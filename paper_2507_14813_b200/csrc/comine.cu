@@ -6,19 +6,28 @@
 //       time from a global atomic queue ("distributes these
 //       candidate edges across warps"), then runs one depth-first co-mining
 //       search per root along the MG-Tree table (Algorithm 3):
-//         - window location: lane-cooperative 32-ary search for the first entry
-//           with time rank > tr_prev in the anchor list (Algo 1 l.210-214);
-//         - candidate filter: lane i takes window entry i (coalesced 8-byte
-//           loads); the entry's neighbour is classified against the warp-uniform
-//           register map m2g (which mapped motif vertex it equals, or NEW); every
-//           child of the anchor group tests its structural constraint with one
-//           compare and a __ballot_sync (Algo 1 l.219 + full injectivity R4) --
-//           the paper's predicated / LUT-simplified checks;
-//         - completion children add __popc(mask) to a per-block counter
-//           (count[Q_N]++, Algo 3 l.661) without descending; inner children
-//           push a frame on the per-warp shared-memory DFS stack and descend
-//           with the candidate as the new partial match (Algo 3 l.665-669).
-//       Per-block shared counters are flushed once per block.
+//         - window location (Algo 1 l.210-214): the edge matched at the current
+//           node carries successor pointers P(e) -- the first position after t_e
+//           in out(src), in(dst), out(dst), in(src) -- so a window anchored at one
+//           of its endpoints starts with no search; lists are sentinel-terminated so
+//           the window ends on "time rank > hi(root)" alone.  Other anchors use the
+//           root edge's pointers as a lower bound, or a lane-cooperative 32-ary search;
+//         - candidate filter: lane i takes window entry i (coalesced 8-byte loads);
+//           the entry's neighbour is classified against the warp-uniform register
+//           map m2g (which mapped motif vertex it is, or NEW); each child of the anchor
+//           group tests its structural constraint with one compare + __ballot_sync
+//           (Algo 1 l.219 + full injectivity, reading R4) -- the paper's predicated /
+//           LUT-simplified checks;
+//         - completion children add __popc(mask) to a lane-resident counter
+//           (count[Q_N]++, Algo 3 l.661) without descending; inner children push a
+//           frame on the per-warp shared-memory DFS stack and descend with the
+//           candidate as the new partial match (Algo 3 l.665-669);
+//         - dynamic load balance (PAPER.md:758-774 inter-warp balancing, 893-904
+//           multi-offload): once warps go idle, a busy warp that reaches the next batch
+//           of a long window fans the rest of the window out as chunk contexts in a
+//           global queue (and the node's remaining anchor groups as one more context).
+//       Counters are reduced per block in shared memory, then flushed once per
+//       block with 64-bit atomics ("context ... maintained locally").
 // All arithmetic is integer (u32 ids and time ranks, i64 timestamps, u64 counts).
 #include <cuda_runtime.h>
 
@@ -36,26 +45,52 @@ constexpr int kBlock = kWarps * 32;
 constexpr int kMaxDepth = MAYURA_MAX_EDGES;  // frames 0..max_edges-2
 constexpr int kMaxGroupChildren = MAYURA_MAX_V + 1;
 constexpr unsigned kFull = 0xffffffffu;
+constexpr uint32_t kNone = 0xffffffffu;
+constexpr int kCtxWords = 32;               // one context = 128 bytes
+constexpr uint32_t kCtxCap = 1u << 20;      // contexts per launch (128 MiB)
 enum { S_GROUP = 0, S_BATCH = 1, S_ITER = 2 };
-enum { ST_ROOTS, ST_NODES, ST_WINDOWS, ST_ENTRIES, ST_PROBES, ST_BATCHES, ST_BYTES, ST_MATCHES, ST_N };
+enum { ST_ROOTS, ST_NODES, ST_WINDOWS, ST_ENTRIES, ST_PROBES, ST_BATCHES, ST_BYTES, ST_MATCHES,
+       ST_OFFLOADS, ST_CONTEXTS, ST_N };
+// load-balancer words (zeroed by window_end_kernel)
+enum { LB_ROOT = 0, LB_TAIL = 1, LB_HEAD = 2, LB_IDLE = 3, LB_WORK = 4, LB_N = 8 };
 
 struct KParams {
     const uint32_t *src, *dst, *tr, *hi;
-    const uint32_t *out_off, *in_off;
-    const uint2 *out_ent, *in_ent;
+    const uint4 *eptr;                 // P(e) per edge id
+    const uint32_t *out_off, *in_off;  // list x = [off[x], off[x+1]-1), sentinel at off[x+1]-1
+    const uint2 *out_ent, *in_ent;     // (tr, nbr)
+    const uint4 *out_ptr, *in_ptr;     // P(e) of each entry's edge
     const DNode *nodes;
     const DGroup *groups;
     const uint32_t *motif_node;
     uint32_t n_nodes, n_groups, n_motifs;
     uint32_t r0, n_roots;
-    uint32_t *queue;
+    uint32_t *lb;
+    uint32_t *ctx;
+    uint32_t ctx_cap, epoch;
     unsigned long long *counts;
     unsigned long long *stats;
 };
 
-struct Frame {  // one per warp per DFS depth (shared memory)
-    uint32_t node, g, g_end, tr_prev, nv, kind, pos, end, batch, ci, mask, c_end;
+struct __align__(16) Frame {  // one per warp per DFS depth (shared memory), 3 x 16 bytes
+    uint32_t node_g, ci, tr_prev, pos;
+    uint32_t batch, mask, lim, g_end;
+    uint4 P;
 };
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 template <int MAXV>
 __device__ __forceinline__ uint32_t m2g_get(const uint32_t (&m)[MAXV], uint32_t i) {
@@ -77,23 +112,71 @@ __device__ __forceinline__ uint32_t classify(const uint32_t (&m)[MAXV], uint32_t
     for (int k = 0; k < MAXV; k++) c = ((uint32_t)k < nv && m[k] == x) ? (uint32_t)k : c;
     return c;
 }
+__device__ __forceinline__ uint32_t pick(const uint4 &v, uint32_t k) {
+    return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ uint4 shfl4(const uint4 &v, int src) {
+    return make_uint4(__shfl_sync(kFull, v.x, src), __shfl_sync(kFull, v.y, src), __shfl_sync(kFull, v.z, src),
+                      __shfl_sync(kFull, v.w, src));
+}
 
-// Coarse lane-cooperative 32-ary search: returns lo' <= first index in [lo, end) whose
-// time rank exceeds tr_prev, with (first - lo') < 32, so the first 32-entry batch
-// from lo' (or its successor) reaches the window.  One sample load per lane per step.
+// Write one search context (lane l writes word l; word 31 = publication flag, written later):
+// [0] node | group << 16 (kNone = no-op), [1] window position (kNone = start the group fresh),
+// [2] position limit, [3] tr_prev, [4] hi(root), [5..8] P, [9..12] R, [13..] m2g.
+template <int MAXV>
+__device__ __forceinline__ void put_ctx(uint32_t *slot, int lane, uint32_t w0, uint32_t w1, uint32_t w2,
+                                        uint32_t w3, uint32_t w4, const uint4 &P, const uint4 &R,
+                                        const uint32_t (&m2g)[MAXV]) {
+    uint32_t v;
+    switch (lane) {
+        case 0: v = w0; break;
+        case 1: v = w1; break;
+        case 2: v = w2; break;
+        case 3: v = w3; break;
+        case 4: v = w4; break;
+        case 5: v = P.x; break;
+        case 6: v = P.y; break;
+        case 7: v = P.z; break;
+        case 8: v = P.w; break;
+        case 9: v = R.x; break;
+        case 10: v = R.y; break;
+        case 11: v = R.z; break;
+        case 12: v = R.w; break;
+        default: v = (lane - 13 < MAXV) ? m2g_get<MAXV>(m2g, lane - 13) : 0u; break;
+    }
+    if (lane < 31) slot[lane] = v;
+}
+// Make contexts [base, base+n) visible: every lane fences its own stores; lane 0 adds the
+// published contexts to the work counter (so "work == 0" implies an empty queue), then sets
+// the flags.
+__device__ __forceinline__ void publish_ctx(uint32_t *ctx, uint32_t cap, uint32_t base, uint32_t n, uint32_t epoch,
+                                            uint32_t *work, int lane) {
+    __syncwarp();
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+        const uint32_t npub = base >= cap ? 0u : min(n, cap - base);
+        if (npub) atomicAdd(work, npub);
+        for (uint32_t j = 0; j < npub; j++) st_release(ctx + (size_t)(base + j) * 32 + 31, epoch);
+    }
+}
+
+// Lane-cooperative 32-ary search: returns lo' <= (first index in [lo, end) whose key exceeds
+// x) with that index - lo' < 32, so the 32-entry batch at lo' reaches it.  key(i) = time rank
+// of list entry i (kind OUT/IN) or of edge i (GLOBAL).  One sample load per lane per step.
 template <bool STATS>
-__device__ __forceinline__ uint32_t locate(uint32_t kind, const uint2 *__restrict__ ent,
+__device__ __forceinline__ uint32_t locate(bool global, const uint2 *__restrict__ ent,
                                            const uint32_t *__restrict__ trg, uint32_t lo, uint32_t end,
-                                           uint32_t tr_prev, int lane, unsigned long long &probes) {
+                                           uint32_t x, int lane, unsigned long long &probes) {
     uint32_t hi = end;
     while (hi - lo > 32) {
         const uint32_t n = hi - lo;
         const uint32_t step = (n + 31) >> 5;
         const uint32_t i = (uint32_t)lane * step;
-        uint32_t key = 0xffffffffu;
-        if (i < n) key = (kind == ANCHOR_GLOBAL) ? __ldg(trg + lo + i) : __ldg(&ent[lo + i].x);
+        uint32_t key = kNone;
+        if (i < n) key = global ? __ldg(trg + lo + i) : __ldg(&ent[lo + i].x);
         if (STATS) probes++;
-        const unsigned b = __ballot_sync(kFull, key > tr_prev);
+        const unsigned b = __ballot_sync(kFull, key > x);
         if (b == 0) {
             lo += 31 * step + 1;
         } else {
@@ -107,14 +190,14 @@ __device__ __forceinline__ uint32_t locate(uint32_t kind, const uint2 *__restric
     return lo;
 }
 
-template <int MAXV, bool STATS>
+template <int MAXV, int CNT, bool STATS>
 __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    DNode *s_nodes = reinterpret_cast<DNode *>(smem);
+    Frame *s_frames = reinterpret_cast<Frame *>(smem);
+    unsigned long long *s_cnt = reinterpret_cast<unsigned long long *>(s_frames + kWarps * kMaxDepth);
+    DNode *s_nodes = reinterpret_cast<DNode *>(s_cnt + p.n_nodes);
     DGroup *s_groups = reinterpret_cast<DGroup *>(s_nodes + p.n_nodes);
-    unsigned long long *s_cnt = reinterpret_cast<unsigned long long *>(s_groups + p.n_groups);
-    Frame *s_frames = reinterpret_cast<Frame *>(s_cnt + p.n_nodes);
-    uint32_t *s_masks = reinterpret_cast<uint32_t *>(s_frames + kWarps * kMaxDepth);
+    uint32_t *s_masks = reinterpret_cast<uint32_t *>(s_groups + p.n_groups);
 
     for (uint32_t i = threadIdx.x; i < p.n_nodes; i += blockDim.x) {
         s_nodes[i] = p.nodes[i];
@@ -126,142 +209,367 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     Frame *F = s_frames + warp * kMaxDepth;
     uint32_t *MS = s_masks + warp * kMaxDepth * kMaxGroupChildren;
-    const DNode root = s_nodes[0];
+    unsigned long long cnt[CNT > 0 ? CNT : 1];
+#pragma unroll
+    for (int s = 0; s < (CNT > 0 ? CNT : 1); s++) cnt[s] = 0;
     unsigned long long st[ST_N];
 #pragma unroll
     for (int i = 0; i < ST_N; i++) st[i] = 0;
 
-    for (;;) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(p.queue, 32u);
-        base = __shfl_sync(kFull, base, 0);
-        if (base >= p.n_roots) break;
-        const bool valid = base + lane < p.n_roots;
-        const uint32_t r = p.r0 + base + lane;
-        uint32_t rs = 0, rd = 0, rt = 0, rh = 0;
-        if (valid) {
-            rs = __ldg(p.src + r);
-            rd = __ldg(p.dst + r);
-            rt = __ldg(p.tr + r);
-            rh = __ldg(p.hi + r);
-        }
-        unsigned ok = __ballot_sync(kFull, valid && rs != rd);  // a self-loop never matches 0->1
-        if (STATS) {
-            const unsigned vm = __ballot_sync(kFull, valid);
-            if (lane == 0) {
-                st[ST_ROOTS] += __popc(ok);
-                st[ST_BYTES] += 16ull * __popc(vm);
-            }
-        }
-        if ((root.flags & NODE_COMPLETION) && lane == 0 && ok) {
-            atomicAdd(&s_cnt[0], (unsigned long long)__popc(ok));
-            if (STATS) st[ST_MATCHES] += __popc(ok);
-        }
-        if (!(root.flags & NODE_INNER)) continue;
-
-        while (ok) {
-            const int j = __ffs(ok) - 1;
-            ok &= ok - 1;
-            uint32_t m2g[MAXV];
+    // counter of trie node c (warp-uniform c, m): lane c%32 owns it (CNT > 0) or shared memory
+    auto count = [&](uint32_t c, unsigned m) {
+        if (CNT == 0) {
+            if (lane == 0 && m) atomicAdd(&s_cnt[c], (unsigned long long)__popc(m));
+        } else {
 #pragma unroll
-            for (int k = 0; k < MAXV; k++) m2g[k] = 0;
-            m2g[0] = __shfl_sync(kFull, rs, j);
-            m2g[1] = __shfl_sync(kFull, rd, j);
-            const uint32_t h = __shfl_sync(kFull, rh, j);
-            uint32_t tr_prev = __shfl_sync(kFull, rt, j);
+            for (int s = 0; s < (CNT > 0 ? CNT : 1); s++)
+                if (c == (uint32_t)(lane + 32 * s)) cnt[s] += __popc(m);
+        }
+        if (STATS && lane == 0) st[ST_MATCHES] += __popc(m);
+    };
 
-            int depth = 0;
-            uint32_t node = 0, nv = 2, g = root.group_begin, g_end = root.group_end;
-            uint32_t kind = 0, pos = 0, end = 0, batch = 0, ci = 0, mask = 0, c_end = 0;
-            uint32_t etr = 0, e1 = 0, e2 = 0;  // this lane's batch entry: time rank, neighbour / (src, dst)
-            int state = S_GROUP;
-            if (STATS && lane == 0) st[ST_NODES]++;
+    const DNode root = s_nodes[0];
+    bool roots_done = false, idle = false;
+    uint32_t ticket = kNone;  // lane 0: claimed queue slot not yet published
 
+    // ---------------------------------------------------------------- DFS state
+    uint32_t m2g[MAXV];
+    uint4 R, P;                    // successor pointers of the root edge / the node's edge
+    uint32_t h = 0, tr_prev = 0, node = 0, nv = 2, g = 0, g_end = 0, kind = 0, pos = 0, lim = kNone;
+    uint32_t batch = 0, ci = 0, c_end = 0, mask = 0, nbatch = 0;
+    int depth = 0, state = S_GROUP;
+    uint32_t etr = 0, e1 = 0, e2 = 0;  // this lane's batch entry: time rank, neighbour / (src, dst)
+    uint4 ep = make_uint4(0, 0, 0, 0); // P of this lane's entry edge
+
+    for (;;) {
+        // ------------------------------------------------------- acquire work
+        uint32_t chunk_base = kNone, ctx_slot = kNone;
+        bool quit = false;
+        if (!roots_done) {
+            uint32_t b = 0;
+            if (lane == 0) {
+                b = atomicAdd(p.lb + LB_ROOT, 32u);
+                if (b < p.n_roots) atomicAdd(p.lb + LB_WORK, 1u);
+            }
+            b = __shfl_sync(kFull, b, 0);
+            if (b < p.n_roots) chunk_base = b;
+            else roots_done = true;
+        }
+        if (chunk_base == kNone) {
+            // context phase: take a ticket (queue slot) and wait for it to be published, or exit
+            // once LB_WORK -- warps holding work + published contexts not yet finished -- is 0
+            uint32_t got = kNone, ex = 0;
+            if (lane == 0) {
+                if (!idle) {
+                    atomicAdd(p.lb + LB_IDLE, 1u);
+                    idle = true;
+                }
+                if (ticket == kNone) ticket = atomicAdd(p.lb + LB_HEAD, 1u);
+                for (int spin = 0;; spin++) {
+                    if (ticket < p.ctx_cap &&
+                        ld_acquire(p.ctx + (size_t)ticket * kCtxWords + (kCtxWords - 1)) == p.epoch) {
+                        got = ticket;
+                        ticket = kNone;
+                        break;
+                    }
+                    if (ld_acquire(p.lb + LB_WORK) == 0) {
+                        ex = 1;
+                        break;
+                    }
+                    __nanosleep(spin < 4 ? 32 : 200);
+                }
+                if (got != kNone) {
+                    atomicSub(p.lb + LB_IDLE, 1u);
+                    idle = false;
+                }
+            }
+            got = __shfl_sync(kFull, got, 0);
+            ex = __shfl_sync(kFull, ex, 0);
+            idle = __shfl_sync(kFull, (int)idle, 0) != 0;
+            if (ex) quit = true;
+            else ctx_slot = got;
+        }
+        if (quit) break;
+
+        // ---------------------------------------------- root chunk: 32 roots
+        uint32_t rs = 0, rd = 0, rt = 0, rh = 0;
+        uint4 rp = make_uint4(0, 0, 0, 0);
+        unsigned pending = 0;
+        if (chunk_base != kNone) {
+            const bool valid = chunk_base + lane < p.n_roots;
+            const uint32_t r = p.r0 + chunk_base + lane;
+            if (valid) {
+                rs = __ldg(p.src + r);
+                rd = __ldg(p.dst + r);
+                rt = __ldg(p.tr + r);
+                rh = __ldg(p.hi + r);
+                if (root.flags & NODE_INNER) rp = __ldg(p.eptr + r);
+            }
+            pending = __ballot_sync(kFull, valid && rs != rd);  // a self-loop never matches 0->1
+            if (STATS) {
+                const unsigned vm = __ballot_sync(kFull, valid);
+                if (lane == 0) {
+                    st[ST_ROOTS] += __popc(pending);
+                    st[ST_BYTES] += 16ull * __popc(vm) + ((root.flags & NODE_INNER) ? 16ull * __popc(pending) : 0);
+                }
+            }
+            if (root.flags & NODE_COMPLETION) count(0, pending);
+            if (!(root.flags & NODE_INNER)) pending = 0;
+        }
+
+        // one search per pending root (or one context)
+        for (;;) {
+            if (chunk_base != kNone) {
+                if (!pending) break;
+                const int j = __ffs(pending) - 1;
+                pending &= pending - 1;
+                if (pending) {
+                    // idle warps exist: hand this chunk's other pending roots to the queue
+                    uint32_t n_idle = 0;
+                    if (lane == 0) n_idle = ld_relaxed(p.lb + LB_IDLE);
+                    n_idle = __shfl_sync(kFull, n_idle, 0);
+                    if (n_idle > 0) {
+                        const uint32_t total = __popc(pending);
+                        uint32_t base = 0;
+                        if (lane == 0) base = atomicAdd(p.lb + LB_TAIL, total);
+                        base = __shfl_sync(kFull, base, 0);
+                        const bool fits = base + total <= p.ctx_cap;
+                        unsigned rest = pending;
+                        for (uint32_t q = 0; q < total && base + q < p.ctx_cap; q++) {
+                            const int b = __ffs(rest) - 1;
+                            rest &= rest - 1;
+                            uint32_t rm[MAXV];
+#pragma unroll
+                            for (int k = 0; k < MAXV; k++) rm[k] = 0;
+                            rm[0] = __shfl_sync(kFull, rs, b);
+                            rm[1] = __shfl_sync(kFull, rd, b);
+                            const uint4 rr = shfl4(rp, b);
+                            put_ctx<MAXV>(p.ctx + (size_t)(base + q) * kCtxWords, lane,
+                                          fits ? (uint32_t)root.group_begin << 16 : kNone, kNone, kNone,
+                                          __shfl_sync(kFull, rt, b), __shfl_sync(kFull, rh, b), rr, rr, rm);
+                        }
+                        publish_ctx(p.ctx, p.ctx_cap, base, total, p.epoch, p.lb + LB_WORK, lane);
+                        if (fits) {
+                            pending = 0;
+                            if (STATS && lane == 0) st[ST_OFFLOADS]++;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < MAXV; k++) m2g[k] = 0;
+                m2g[0] = __shfl_sync(kFull, rs, j);
+                m2g[1] = __shfl_sync(kFull, rd, j);
+                h = __shfl_sync(kFull, rh, j);
+                tr_prev = __shfl_sync(kFull, rt, j);
+                R = shfl4(rp, j);
+                P = R;
+                node = 0; nv = 2; g = root.group_begin; g_end = root.group_end;
+                lim = kNone; depth = 0; state = S_GROUP;
+                if (STATS && lane == 0) st[ST_NODES]++;
+            } else {
+                if (ctx_slot == kNone) break;
+                uint32_t w = 0;
+                if (ctx_slot < p.ctx_cap) {
+                    if (lane == 0)
+                        while (ld_acquire(p.ctx + (size_t)ctx_slot * kCtxWords + (kCtxWords - 1)) != p.epoch)
+                            __nanosleep(32);
+                    __syncwarp();
+                    w = __ldcg(p.ctx + (size_t)ctx_slot * kCtxWords + lane);
+                } else {
+                    w = kNone;
+                }
+                ctx_slot = kNone;
+                const uint32_t w0 = __shfl_sync(kFull, w, 0);
+                if (w0 == kNone) continue;  // no-op context (overflowed reservation)
+                node = w0 & 0xffffu;
+                g = w0 >> 16;
+                pos = __shfl_sync(kFull, w, 1);
+                lim = __shfl_sync(kFull, w, 2);
+                tr_prev = __shfl_sync(kFull, w, 3);
+                h = __shfl_sync(kFull, w, 4);
+                P = make_uint4(__shfl_sync(kFull, w, 5), __shfl_sync(kFull, w, 6), __shfl_sync(kFull, w, 7),
+                               __shfl_sync(kFull, w, 8));
+                R = make_uint4(__shfl_sync(kFull, w, 9), __shfl_sync(kFull, w, 10), __shfl_sync(kFull, w, 11),
+                               __shfl_sync(kFull, w, 12));
+#pragma unroll
+                for (int k = 0; k < MAXV; k++) m2g[k] = __shfl_sync(kFull, w, 13 + k);
+                const DNode dn = s_nodes[node];
+                nv = dn.nv;
+                g_end = (lim != kNone) ? g + 1 : dn.group_end;
+                depth = 0;
+                if (pos == kNone) {
+                    state = S_GROUP;
+                } else {
+                    kind = s_groups[g].kind;
+                    nbatch = 1;  // a continuation: may split again
+                    state = S_BATCH;
+                }
+                if (STATS && lane == 0) st[ST_CONTEXTS]++;
+            }
+
+            // ---------------------------------------------------- the search
             for (;;) {
                 if (state == S_GROUP) {
-                    if (g == g_end) {  // all children groups of `node` done: pop
+                    if (g == g_end) {  // all anchor groups of `node` done: pop
                         if (depth == 0) break;
                         --depth;
                         __syncwarp();
                         const Frame f = F[depth];
-                        node = f.node; g = f.g; g_end = f.g_end; tr_prev = f.tr_prev; nv = f.nv;
-                        kind = f.kind; pos = f.pos; end = f.end; batch = f.batch; ci = f.ci;
-                        mask = f.mask; c_end = f.c_end;
+                        node = f.node_g & 0xffffu; g = f.node_g >> 16; ci = f.ci; tr_prev = f.tr_prev;
+                        pos = f.pos; batch = f.batch; mask = f.mask; lim = f.lim; g_end = f.g_end; P = f.P;
+                        const DGroup G = s_groups[g];
+                        nv = s_nodes[node].nv;
+                        kind = G.kind; c_end = G.child_end;
                         const uint32_t idx = batch + lane;
-                        if (idx < end) {
-                            if (kind == ANCHOR_GLOBAL) {
-                                etr = __ldg(p.tr + idx); e1 = __ldg(p.src + idx); e2 = __ldg(p.dst + idx);
-                            } else {
-                                const uint2 e = __ldg((kind == ANCHOR_OUT ? p.out_ent : p.in_ent) + idx);
-                                etr = e.x; e1 = e.y;
-                            }
+                        if (kind == ANCHOR_GLOBAL) {
+                            etr = __ldg(p.tr + idx); e1 = __ldg(p.src + idx); e2 = __ldg(p.dst + idx);
+                            ep = __ldg(p.eptr + idx);
+                        } else {
+                            const uint2 e = __ldg((kind == ANCHOR_OUT ? p.out_ent : p.in_ent) + idx);
+                            etr = e.x; e1 = e.y;
+                            ep = __ldg((kind == ANCHOR_OUT ? p.out_ptr : p.in_ptr) + idx);
                         }
                         state = S_ITER;
-                        continue;
-                    }
-                    const DGroup G = s_groups[g];
-                    kind = G.kind;
-                    if (kind == ANCHOR_GLOBAL) {
-                        pos = tr_prev;  // first edge of the previous edge's tie group
-                        end = h + 1;
                     } else {
-                        const uint32_t x = m2g_get<MAXV>(m2g, G.anchor);
-                        const uint32_t *off = (kind == ANCHOR_OUT) ? p.out_off : p.in_off;
-                        pos = __ldg(off + x);
-                        end = __ldg(off + x + 1);
-                        if (STATS && lane == 0) st[ST_BYTES] += 8;
+                        const DGroup G = s_groups[g];
+                        kind = G.kind;
+                        nbatch = 0;
+                        if (G.start < START_R0) {
+                            pos = pick(P, G.start);
+                        } else if (G.start < START_SEARCH) {
+                            pos = pick(R, G.start - START_R0);
+                        } else if (G.start == START_SEARCH) {
+                            const uint32_t x = m2g_get<MAXV>(m2g, G.anchor);
+                            const uint32_t *off = (kind == ANCHOR_OUT) ? p.out_off : p.in_off;
+                            const uint32_t lo = __ldg(off + x), end = __ldg(off + x + 1) - 1;
+                            pos = locate<STATS>(false, kind == ANCHOR_OUT ? p.out_ent : p.in_ent, p.tr, lo, end,
+                                                tr_prev, lane, st[ST_PROBES]);
+                            if (STATS && lane == 0) st[ST_BYTES] += 8;
+                        } else {  // GLOBAL: edge ids (tie group of the previous edge, hi(root)]
+                            pos = locate<STATS>(true, nullptr, p.tr, tr_prev, h + 1, tr_prev, lane, st[ST_PROBES]);
+                        }
+                        // a fresh window is bounded by hi(root) alone (edge ids for GLOBAL);
+                        // chunk contexts enter S_BATCH directly with their own limit
+                        lim = (kind == ANCHOR_GLOBAL) ? h + 1 : kNone;
+                        if (STATS && lane == 0) st[ST_WINDOWS]++;
+                        state = S_BATCH;
                     }
-                    pos = locate<STATS>(kind, kind == ANCHOR_OUT ? p.out_ent : p.in_ent, p.tr, pos, end,
-                                        tr_prev, lane, st[ST_PROBES]);
-                    if (STATS && lane == 0) st[ST_WINDOWS]++;
-                    state = S_BATCH;
                 }
                 if (state == S_BATCH) {
-                    if (pos >= end) {
+                    const DGroup G = s_groups[g];
+                    if (pos >= lim) {
                         ++g;
                         state = S_GROUP;
                         continue;
                     }
-                    batch = pos;
-                    const uint32_t idx = pos + lane;
-                    bool in = idx < end;
-                    etr = 0xffffffffu;
-                    if (in) {
-                        if (kind == ANCHOR_GLOBAL) {
-                            etr = __ldg(p.tr + idx); e1 = __ldg(p.src + idx); e2 = __ldg(p.dst + idx);
-                        } else {
-                            const uint2 e = __ldg((kind == ANCHOR_OUT ? p.out_ent : p.in_ent) + idx);
-                            etr = e.x; e1 = e.y;
+                    // ---- dynamic load balance: split the rest of a long window when warps idle
+                    if (nbatch > 0) {
+                        uint32_t n_idle = 0;
+                        if (lane == 0) n_idle = ld_relaxed(p.lb + LB_IDLE);
+                        n_idle = __shfl_sync(kFull, n_idle, 0);
+                        if (n_idle > 0) {
+                            // window end: first position in [pos, list end) with time rank > h
+                            uint32_t wend;
+                            if (kind == ANCHOR_GLOBAL) {
+                                wend = lim;
+                            } else {
+                                const uint32_t x = m2g_get<MAXV>(m2g, G.anchor);
+                                const uint32_t *off = (kind == ANCHOR_OUT) ? p.out_off : p.in_off;
+                                const uint2 *ent = (kind == ANCHOR_OUT) ? p.out_ent : p.in_ent;
+                                const uint32_t end = __ldg(off + x + 1);  // one past the sentinel
+                                uint32_t lo = locate<STATS>(false, ent, p.tr, pos, end, h, lane, st[ST_PROBES]);
+                                const uint32_t idx = lo + lane;
+                                const uint32_t k2 = idx < end ? __ldg(&ent[idx].x) : kNone;
+                                const unsigned b = __ballot_sync(kFull, k2 > h);
+                                wend = b ? lo + (uint32_t)(__ffs(b) - 1) : end;
+                                wend = min(wend, lim);
+                            }
+                            const uint32_t nb = wend > pos ? (wend - pos + 31) / 32 : 0;
+                            uint32_t per = G.n_inner ? 1u : 4u;
+                            uint32_t nctx = (nb + per - 1) / per;
+                            if (nctx > 32) {
+                                per = (nb + 31) / 32;
+                                nctx = (nb + per - 1) / per;
+                            }
+                            const uint32_t extra = (g + 1 < g_end) ? 1u : 0u;
+                            const uint32_t total = nctx + extra;
+                            if (nb >= 2) {
+                                uint32_t base = 0;
+                                if (lane == 0) base = atomicAdd(p.lb + LB_TAIL, total);
+                                base = __shfl_sync(kFull, base, 0);
+                                const bool fits = base + total <= p.ctx_cap;
+                                for (uint32_t j = 0; j < total && base + j < p.ctx_cap; j++) {
+                                    const bool chunk = j < nctx;
+                                    put_ctx<MAXV>(p.ctx + (size_t)(base + j) * kCtxWords, lane,
+                                                  fits ? (node | ((chunk ? g : g + 1) << 16)) : kNone,
+                                                  chunk ? pos + j * per * 32 : kNone,
+                                                  chunk ? min(wend, pos + (j + 1) * per * 32) : kNone, tr_prev, h,
+                                                  P, R, m2g);
+                                }
+                                publish_ctx(p.ctx, p.ctx_cap, base, total, p.epoch, p.lb + LB_WORK, lane);
+                                if (fits) {
+                                    if (STATS && lane == 0) st[ST_OFFLOADS]++;
+                                    g = g_end;  // this node's remaining work now lives in the queue
+                                    state = S_GROUP;
+                                    continue;
+                                }
+                            }
                         }
                     }
-                    in = in && etr <= h;
-                    const bool w = in && etr > tr_prev;
-                    const bool more = __shfl_sync(kFull, (int)in, 31) != 0;
-                    pos = more ? pos + 32 : end;
+                    // ---- load one batch of 32 window entries
+                    const uint32_t idx = pos + lane;
+                    bool fail;
+                    const bool inner = G.n_inner != 0;
+                    if (kind == ANCHOR_GLOBAL) {
+                        fail = idx >= lim;
+                        etr = kNone;
+                        if (!fail) {
+                            etr = __ldg(p.tr + idx); e1 = __ldg(p.src + idx); e2 = __ldg(p.dst + idx);
+                            if (inner) ep = __ldg(p.eptr + idx);
+                        }
+                    } else {
+                        const uint2 e = __ldg((kind == ANCHOR_OUT ? p.out_ent : p.in_ent) + idx);
+                        etr = e.x; e1 = e.y;
+                        if (inner) ep = __ldg((kind == ANCHOR_OUT ? p.out_ptr : p.in_ptr) + idx);
+                        fail = etr > h || idx >= lim;
+                    }
+                    const unsigned fm = __ballot_sync(kFull, fail);
+                    const unsigned inmask = fm ? ((1u << (__ffs(fm) - 1)) - 1u) : kFull;  // lanes before the window end
+                    const bool w = ((inmask >> lane) & 1u) && etr > tr_prev;
+                    const unsigned wm = __ballot_sync(kFull, w);
+                    batch = pos;
+                    pos = fm ? kNone : pos + 32;
+                    ++nbatch;
+                    if (STATS && lane == 0) {
+                        st[ST_BATCHES]++;
+                        st[ST_ENTRIES] += __popc(wm);
+                        st[ST_BYTES] += (kind == ANCHOR_GLOBAL ? 12ull : 8ull) * (__popc(wm) + (fm ? 1 : 0)) +
+                                        (inner ? 16ull * __popc(wm) : 0ull);
+                    }
+                    if (wm == 0) {
+                        // forward skip from a lower-bound start: the whole batch precedes the window
+                        const uint32_t last = __shfl_sync(kFull, etr, 31);
+                        if (!fm && G.start >= START_R0 && G.start < START_SEARCH && nbatch >= 2 && last <= tr_prev) {
+                            const uint32_t x = m2g_get<MAXV>(m2g, G.anchor);
+                            const uint32_t *off = (kind == ANCHOR_OUT) ? p.out_off : p.in_off;
+                            const uint32_t end = __ldg(off + x + 1) - 1;
+                            pos = locate<STATS>(false, kind == ANCHOR_OUT ? p.out_ent : p.in_ent, p.tr, pos, end,
+                                                tr_prev, lane, st[ST_PROBES]);
+                            nbatch = 0;
+                        }
+                        continue;
+                    }
                     uint32_t cls;
                     if (kind == ANCHOR_GLOBAL)
-                        cls = (classify<MAXV>(m2g, nv, e1) == CLS_NEW && classify<MAXV>(m2g, nv, e2) == CLS_NEW &&
-                               e1 != e2) ? CLS_NEW : 0xFEu;
+                        cls = (e1 != e2 && classify<MAXV>(m2g, nv, e1) == CLS_NEW &&
+                               classify<MAXV>(m2g, nv, e2) == CLS_NEW) ? CLS_NEW : 0xFEu;
                     else
                         cls = classify<MAXV>(m2g, nv, e1);
-                    const DGroup G = s_groups[g];
-                    if (STATS) {
-                        const unsigned wm = __ballot_sync(kFull, w);
-                        if (lane == 0) {
-                            st[ST_BATCHES]++;
-                            st[ST_ENTRIES] += __popc(wm);
-                            st[ST_BYTES] += (kind == ANCHOR_GLOBAL ? 12ull : 8ull) *
-                                            (__popc(wm) + (more ? 0 : 1));
-                        }
-                    }
                     bool any_inner = false;
                     for (uint32_t c = G.child_begin; c < G.child_end; ++c) {
                         const DNode dn = s_nodes[c];
                         const unsigned mc = __ballot_sync(kFull, w && cls == dn.want);
-                        if ((dn.flags & NODE_COMPLETION) && mc && lane == 0) {
-                            atomicAdd(&s_cnt[c], (unsigned long long)__popc(mc));
-                            if (STATS) st[ST_MATCHES] += __popc(mc);
-                        }
+                        if (dn.flags & NODE_COMPLETION) count(c, mc);
                         if (dn.flags & NODE_INNER) {
                             if (lane == 0) MS[depth * kMaxGroupChildren + (c - G.child_begin)] = mc;
                             any_inner |= (mc != 0);
@@ -274,7 +582,7 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
                     mask = (s_nodes[ci].flags & NODE_INNER) ? MS[depth * kMaxGroupChildren] : 0u;
                     state = S_ITER;
                 }
-                // S_ITER: next (inner child, candidate) pair of the current batch
+                // ---- S_ITER: next (inner child, candidate) pair of the current batch
                 while (mask == 0) {
                     if (++ci >= c_end) break;
                     const uint32_t cb = s_groups[g].child_begin;
@@ -289,10 +597,11 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
                 const uint32_t ctr = __shfl_sync(kFull, etr, b);
                 const uint32_t c1 = __shfl_sync(kFull, e1, b);
                 const uint32_t c2 = __shfl_sync(kFull, e2, b);
+                const uint4 cp = shfl4(ep, b);
                 if (lane == 0) {
                     Frame f;
-                    f.node = node; f.g = g; f.g_end = g_end; f.tr_prev = tr_prev; f.nv = nv; f.kind = kind;
-                    f.pos = pos; f.end = end; f.batch = batch; f.ci = ci; f.mask = mask; f.c_end = c_end;
+                    f.node_g = node | (g << 16); f.ci = ci; f.tr_prev = tr_prev; f.pos = pos;
+                    f.batch = batch; f.mask = mask; f.lim = lim; f.g_end = g_end; f.P = P;
                     F[depth] = f;
                 }
                 const DNode dc = s_nodes[ci];
@@ -300,13 +609,25 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
                 if (dc.n_new == 2) m2g_set<MAXV>(m2g, nv + 1, c2);
                 nv = dc.nv;
                 tr_prev = ctr;
+                P = cp;
                 node = ci;
                 g = dc.group_begin;
                 g_end = dc.group_end;
+                lim = kNone;
                 ++depth;
                 state = S_GROUP;
                 if (STATS && lane == 0) st[ST_NODES]++;
             }
+        }
+        if (lane == 0) atomicSub(p.lb + LB_WORK, 1u);
+    }
+
+    // ---- counters: lanes -> block (shared) -> global, once per block
+    if (CNT > 0) {
+#pragma unroll
+        for (int s = 0; s < (CNT > 0 ? CNT : 1); s++) {
+            const uint32_t c = lane + 32 * s;
+            if (c < p.n_nodes && cnt[s]) atomicAdd(&s_cnt[c], cnt[s]);
         }
     }
     __syncthreads();
@@ -322,13 +643,13 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
 }
 
 // a2: hi[r] = (last edge id e with t[e] <= t[r] + delta), by galloping from r (windows
-// are short) then binary search.  Also zeroes the work-queue cursors and the output
+// are short) then binary search.  Also zeroes the load-balancer words and the output
 // counts of this call, so a co-mining query is exactly two launches.
 __global__ void window_end_kernel(const int64_t *__restrict__ T, uint32_t E, int64_t delta, uint32_t r0,
-                                  uint32_t n_roots, uint32_t *__restrict__ hi, uint32_t *queue, uint32_t n_queue,
+                                  uint32_t n_roots, uint32_t *__restrict__ hi, uint32_t *lb, uint32_t n_lb,
                                   unsigned long long *counts, uint32_t n_counts) {
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
-    if (tid < n_queue) queue[tid] = 0;
+    if (tid < n_lb) lb[tid] = 0;
     if (tid < n_counts) counts[tid] = 0;
     for (uint32_t k = tid; k < n_roots; k += gridDim.x * blockDim.x) {
         const uint32_t r = r0 + k;
@@ -362,8 +683,8 @@ struct DeviceTable {
 };
 
 size_t smem_bytes(uint32_t n_nodes, uint32_t n_groups) {
-    return (size_t)n_nodes * sizeof(DNode) + (size_t)n_groups * sizeof(DGroup) +
-           (size_t)n_nodes * sizeof(unsigned long long) + sizeof(Frame) * kWarps * kMaxDepth +
+    return sizeof(Frame) * kWarps * kMaxDepth + (size_t)n_nodes * sizeof(unsigned long long) +
+           (size_t)n_nodes * sizeof(DNode) + (size_t)n_groups * sizeof(DGroup) +
            sizeof(uint32_t) * kWarps * kMaxDepth * kMaxGroupChildren;
 }
 
@@ -371,15 +692,15 @@ mayura_status cuda_fail(cudaError_t e, const char *what) {
     return fail(MAYURA_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-#define CK(call, what)                                  \
-    do {                                                \
-        cudaError_t e_ = (call);                        \
+#define CK(call, what)                                     \
+    do {                                                   \
+        cudaError_t e_ = (call);                           \
         if (e_ != cudaSuccess) return cuda_fail(e_, what); \
     } while (0)
 
-template <int MAXV, bool STATS>
+template <int MAXV, int CNT, bool STATS>
 cudaError_t launch_comine_t(const KParams &p, size_t smem, cudaStream_t s, int sms) {
-    auto kern = comine_kernel<MAXV, STATS>;
+    auto kern = comine_kernel<MAXV, CNT, STATS>;
     // occupancy is queried once per (kernel instance, shared-memory size, device)
     static std::mutex mu;
     static size_t cached_smem = 0;
@@ -409,27 +730,24 @@ cudaError_t launch_comine_t(const KParams &p, size_t smem, cudaStream_t s, int s
     return cudaGetLastError();
 }
 
-cudaError_t launch_comine(const KParams &p, uint32_t max_vertices, bool stats, cudaStream_t s, int sms) {
+template <int MAXV>
+cudaError_t launch_comine_v(const KParams &p, bool stats, cudaStream_t s, int sms) {
     const size_t smem = smem_bytes(p.n_nodes, p.n_groups);
-    if (stats) {
-        if (max_vertices <= 4) return launch_comine_t<4, true>(p, smem, s, sms);
-        if (max_vertices <= 8) return launch_comine_t<8, true>(p, smem, s, sms);
-        return launch_comine_t<16, true>(p, smem, s, sms);
-    }
-    if (max_vertices <= 4) return launch_comine_t<4, false>(p, smem, s, sms);
-    if (max_vertices <= 8) return launch_comine_t<8, false>(p, smem, s, sms);
-    return launch_comine_t<16, false>(p, smem, s, sms);
+    if (p.n_nodes <= 32)
+        return stats ? launch_comine_t<MAXV, 1, true>(p, smem, s, sms) : launch_comine_t<MAXV, 1, false>(p, smem, s, sms);
+    if (p.n_nodes <= 64)
+        return stats ? launch_comine_t<MAXV, 2, true>(p, smem, s, sms) : launch_comine_t<MAXV, 2, false>(p, smem, s, sms);
+    return stats ? launch_comine_t<MAXV, 0, true>(p, smem, s, sms) : launch_comine_t<MAXV, 0, false>(p, smem, s, sms);
 }
 
-mayura_status upload_table(const Table &t, uint32_t n_motifs, DeviceTable &d, void *&owner) {
-    const size_t bn = t.nodes.size() * sizeof(DNode), bg = t.groups.size() * sizeof(DGroup),
-                 bm = t.motif_node.size() * sizeof(uint32_t);
-    char *buf = nullptr;
-    CK(cudaMalloc(&buf, bn + bg + bm + 16), "cudaMalloc(mgtree table)");
-    CK(cudaMemcpy(buf, t.nodes.data(), bn, cudaMemcpyHostToDevice), "cudaMemcpy(table)");
-    CK(cudaMemcpy(buf + bn, t.groups.data(), bg, cudaMemcpyHostToDevice), "cudaMemcpy(table)");
-    CK(cudaMemcpy(buf + bn + bg, t.motif_node.data(), bm, cudaMemcpyHostToDevice), "cudaMemcpy(table)");
-    owner = buf;
+cudaError_t launch_comine(const KParams &p, uint32_t max_vertices, bool stats, cudaStream_t s, int sms) {
+    if (max_vertices <= 4) return launch_comine_v<4>(p, stats, s, sms);
+    if (max_vertices <= 8) return launch_comine_v<8>(p, stats, s, sms);
+    return launch_comine_v<16>(p, stats, s, sms);
+}
+
+void table_view(const Table &t, uint32_t n_motifs, char *buf, DeviceTable &d) {
+    const size_t bn = t.nodes.size() * sizeof(DNode), bg = t.groups.size() * sizeof(DGroup);
     d.nodes = reinterpret_cast<DNode *>(buf);
     d.groups = reinterpret_cast<DGroup *>(buf + bn);
     d.motif_node = reinterpret_cast<uint32_t *>(buf + bn + bg);
@@ -437,6 +755,18 @@ mayura_status upload_table(const Table &t, uint32_t n_motifs, DeviceTable &d, vo
     d.n_groups = (uint32_t)t.groups.size();
     d.n_motifs = n_motifs;
     d.max_vertices = t.max_vertices;
+}
+
+mayura_status upload_table(const Table &t, uint32_t n_motifs, DeviceTable &d, void *&owner) {
+    const size_t bn = t.nodes.size() * sizeof(DNode), bg = t.groups.size() * sizeof(DGroup),
+                 bm = t.motif_node.size() * sizeof(uint32_t);
+    char *buf = nullptr;
+    CK(cudaMalloc(&buf, bn + bg + bm + 16), "cudaMalloc(mgtree table)");
+    owner = buf;
+    CK(cudaMemcpy(buf, t.nodes.data(), bn, cudaMemcpyHostToDevice), "cudaMemcpy(table)");
+    if (bg) CK(cudaMemcpy(buf + bn, t.groups.data(), bg, cudaMemcpyHostToDevice), "cudaMemcpy(table)");
+    CK(cudaMemcpy(buf + bn + bg, t.motif_node.data(), bm, cudaMemcpyHostToDevice), "cudaMemcpy(table)");
+    table_view(t, n_motifs, buf, d);
     return MAYURA_OK;
 }
 
@@ -445,38 +775,31 @@ void free_tables(mayura_mgtree_s *m) {
         int prev = 0;
         cudaGetDevice(&prev);
         cudaSetDevice(m->dev);
-        for (void *p : m->d_tables) cudaFree(p);
+        for (void *p : m->d_tables)
+            if (p) cudaFree(p);
         cudaSetDevice(prev);
     }
     m->d_tables.clear();
     m->dev = -1;
 }
 
+// Device copies of the group table ([0]) and the single-motif tables ([1..k]), uploaded once
+// per (tree, device) and cached in the tree handle.
 mayura_status ensure_tables(mayura_mgtree_s *m, int dev, std::vector<DeviceTable> &out) {
     if (m->dev != dev) free_tables(m);
     out.resize(1 + m->single.size());
-    std::vector<void *> owners(out.size(), nullptr);
-    // (re)upload each call is cheap but we cache per device
     if (m->dev == dev && m->d_tables.size() == out.size()) {
-        for (size_t i = 0; i < out.size(); i++) {
-            const Table &t = i == 0 ? m->group : m->single[i - 1];
-            char *buf = (char *)m->d_tables[i];
-            const size_t bn = t.nodes.size() * sizeof(DNode), bg = t.groups.size() * sizeof(DGroup);
-            out[i].nodes = reinterpret_cast<DNode *>(buf);
-            out[i].groups = reinterpret_cast<DGroup *>(buf + bn);
-            out[i].motif_node = reinterpret_cast<uint32_t *>(buf + bn + bg);
-            out[i].n_nodes = (uint32_t)t.nodes.size();
-            out[i].n_groups = (uint32_t)t.groups.size();
-            out[i].n_motifs = i == 0 ? m->n_motifs : 1;
-            out[i].max_vertices = t.max_vertices;
-        }
+        for (size_t i = 0; i < out.size(); i++)
+            table_view(i == 0 ? m->group : m->single[i - 1], i == 0 ? m->n_motifs : 1, (char *)m->d_tables[i], out[i]);
         return MAYURA_OK;
     }
+    std::vector<void *> owners(out.size(), nullptr);
     for (size_t i = 0; i < out.size(); i++) {
         const Table &t = i == 0 ? m->group : m->single[i - 1];
         mayura_status s = upload_table(t, i == 0 ? m->n_motifs : 1, out[i], owners[i]);
         if (s != MAYURA_OK) {
-            for (void *p : owners) if (p) cudaFree(p);
+            for (void *p : owners)
+                if (p) cudaFree(p);
             return s;
         }
     }
@@ -504,7 +827,7 @@ int sm_count(int dev) {
     return n > 0 ? n : 1;
 }
 
-// mode 0: co-mine, 1: independent (one launch per motif), stats: instrumented kernel.
+// mode 0: co-mine, 1: independent (one launch per motif); stats: instrumented kernel.
 mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t re, void *stream,
                   uint64_t *counts_out, int on_device, int mode, unsigned long long *stats_host,
                   void *mid_event = nullptr) {
@@ -529,36 +852,49 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
         }
         d_counts = g->d_counts;
     }
+    if (!g->d_ctx) {
+        CK(cudaMalloc(&g->d_ctx, sizeof(uint32_t) * kCtxWords * (size_t)kCtxCap), "cudaMalloc(contexts)");
+        CK(cudaMemset(g->d_ctx, 0, sizeof(uint32_t) * kCtxWords * (size_t)kCtxCap), "cudaMemset(contexts)");
+        g->ctx_cap = kCtxCap;
+        g->device_bytes += sizeof(uint32_t) * kCtxWords * (size_t)kCtxCap;
+    }
     if (stats_host && !g->d_stats) CK(cudaMalloc(&g->d_stats, sizeof(unsigned long long) * ST_N), "cudaMalloc(stats)");
     if (stats_host) CK(cudaMemsetAsync(g->d_stats, 0, sizeof(unsigned long long) * ST_N, s), "cudaMemsetAsync(stats)");
     const uint32_t n_roots = (uint32_t)(re - rb);
-    const uint32_t n_queue = mode == 1 ? k : 1;
+    const size_t n_launch = mode == 1 ? k : 1;
+    const uint32_t n_lb = (uint32_t)(LB_N * n_launch);
     {
         const int threads = 256;
         uint32_t blocks = (n_roots + threads - 1) / threads;
-        const uint32_t minb = (std::max(n_queue, k) + threads - 1) / threads;
+        const uint32_t minb = (std::max(n_lb, k) + threads - 1) / threads;
         blocks = std::max(blocks, minb);
         blocks = std::min<uint32_t>(blocks, 148u * 32u);
         if (blocks == 0) blocks = 1;
         window_end_kernel<<<blocks, threads, 0, s>>>(g->d_t, (uint32_t)g->E, m->delta, (uint32_t)rb, n_roots,
-                                                     g->d_hi, g->d_queue, n_queue, d_counts, k);
+                                                     g->d_hi, g->d_queue, n_lb, d_counts, k);
         CK(cudaGetLastError(), "window_end_kernel launch");
     }
     if (mid_event) CK(cudaEventRecord((cudaEvent_t)mid_event, s), "cudaEventRecord(mid_event)");
     const int sms = sm_count(g->device);
     if (n_roots > 0) {
-        const size_t n_launch = mode == 1 ? k : 1;
         for (size_t i = 0; i < n_launch; i++) {
             const DeviceTable &dt = mode == 1 ? tabs[1 + i] : tabs[0];
             KParams p;
             p.src = g->d_src; p.dst = g->d_dst; p.tr = g->d_tr; p.hi = g->d_hi;
+            p.eptr = reinterpret_cast<const uint4 *>(g->d_eptr);
             p.out_off = g->d_out_off; p.in_off = g->d_in_off;
             p.out_ent = reinterpret_cast<const uint2 *>(g->d_out_ent);
             p.in_ent = reinterpret_cast<const uint2 *>(g->d_in_ent);
+            p.out_ptr = reinterpret_cast<const uint4 *>(g->d_out_ptr);
+            p.in_ptr = reinterpret_cast<const uint4 *>(g->d_in_ptr);
             p.nodes = dt.nodes; p.groups = dt.groups; p.motif_node = dt.motif_node;
             p.n_nodes = dt.n_nodes; p.n_groups = dt.n_groups; p.n_motifs = dt.n_motifs;
             p.r0 = (uint32_t)rb; p.n_roots = n_roots;
-            p.queue = g->d_queue + i;
+            p.lb = g->d_queue + LB_N * i;
+            p.ctx = g->d_ctx;
+            p.ctx_cap = g->ctx_cap;
+            p.epoch = ++g->epoch;
+            if (p.epoch == 0) p.epoch = ++g->epoch;  // 0 marks a never-written slot
             p.counts = d_counts + (mode == 1 ? i : 0);
             p.stats = g->d_stats;
             CK(launch_comine(p, dt.max_vertices, stats_host != nullptr, s, sms), "comine_kernel launch");
@@ -579,16 +915,20 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
 void free_device(mayura_graph_s *g) {
     if (g->device < 0) return;
     DeviceGuard guard(g->device);
-    void *ptrs[] = {g->d_src, g->d_dst, g->d_tr, g->d_hi, g->d_t, g->d_out_off, g->d_in_off,
-                    g->d_out_ent, g->d_in_ent, g->d_queue, g->d_counts, g->d_stats};
+    void *ptrs[] = {g->d_src, g->d_dst, g->d_tr, g->d_hi, g->d_t, g->d_out_off, g->d_in_off, g->d_out_ent,
+                    g->d_in_ent, g->d_eptr, g->d_out_ptr, g->d_in_ptr, g->d_ctx, g->d_queue, g->d_counts,
+                    g->d_stats};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
 
+// Upload h plus `pad` trailing elements filled with byte `fill` (so 32-wide batches never
+// read past the allocation).
 template <typename T>
-mayura_status up(T *&d, const std::vector<T> &h, size_t min_elems, uint64_t &bytes) {
-    const size_t n = std::max(h.size(), min_elems);
+mayura_status up(T *&d, const std::vector<T> &h, size_t min_elems, size_t pad, int fill, uint64_t &bytes) {
+    const size_t n = std::max(h.size(), min_elems) + pad;
     CK(cudaMalloc(&d, sizeof(T) * (n ? n : 1)), "cudaMalloc(graph)");
+    if (n > h.size()) CK(cudaMemset(d, fill, sizeof(T) * n), "cudaMemset(graph)");
     if (!h.empty()) CK(cudaMemcpy(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice), "cudaMemcpy(graph)");
     bytes += sizeof(T) * n;
     return MAYURA_OK;
@@ -635,17 +975,21 @@ extern "C" mayura_status mayura_load_graph(const uint32_t *src, const uint32_t *
         uint64_t bytes = 0;
         std::vector<uint32_t> none;
         const size_t E = (size_t)n_edges;
+        const size_t PADE = 32;  // 32 trailing elements per array
         mayura_status u = MAYURA_OK;
-        if (u == MAYURA_OK) u = up(g->d_src, g->src, 0, bytes);
-        if (u == MAYURA_OK) u = up(g->d_dst, g->dst, 0, bytes);
-        if (u == MAYURA_OK) u = up(g->d_tr, g->tr, 0, bytes);
-        if (u == MAYURA_OK) u = up(g->d_t, g->t, 0, bytes);
-        if (u == MAYURA_OK) u = up(g->d_hi, none, E, bytes);
-        if (u == MAYURA_OK) u = up(g->d_out_off, g->out_off, 0, bytes);
-        if (u == MAYURA_OK) u = up(g->d_in_off, g->in_off, 0, bytes);
-        if (u == MAYURA_OK) u = up(g->d_out_ent, g->out_ent, 0, bytes);
-        if (u == MAYURA_OK) u = up(g->d_in_ent, g->in_ent, 0, bytes);
-        if (u == MAYURA_OK) u = up(g->d_queue, none, MAYURA_MAX_MOTIFS + 1, bytes);
+        if (u == MAYURA_OK) u = up(g->d_src, g->src, 0, PADE, 0, bytes);
+        if (u == MAYURA_OK) u = up(g->d_dst, g->dst, 0, PADE, 0, bytes);
+        if (u == MAYURA_OK) u = up(g->d_tr, g->tr, 0, PADE, 0xFF, bytes);
+        if (u == MAYURA_OK) u = up(g->d_t, g->t, 0, 0, 0, bytes);
+        if (u == MAYURA_OK) u = up(g->d_hi, none, E, PADE, 0, bytes);
+        if (u == MAYURA_OK) u = up(g->d_eptr, g->eptr, 0, 4 * PADE, 0, bytes);
+        if (u == MAYURA_OK) u = up(g->d_out_off, g->out_off, 0, 0, 0, bytes);
+        if (u == MAYURA_OK) u = up(g->d_in_off, g->in_off, 0, 0, 0, bytes);
+        if (u == MAYURA_OK) u = up(g->d_out_ent, g->out_ent, 0, 2 * PADE, 0xFF, bytes);  // sentinel padding
+        if (u == MAYURA_OK) u = up(g->d_in_ent, g->in_ent, 0, 2 * PADE, 0xFF, bytes);
+        if (u == MAYURA_OK) u = up(g->d_out_ptr, g->out_ptr, 0, 4 * PADE, 0, bytes);
+        if (u == MAYURA_OK) u = up(g->d_in_ptr, g->in_ptr, 0, 4 * PADE, 0, bytes);
+        if (u == MAYURA_OK) u = up(g->d_queue, none, (size_t)LB_N * (MAYURA_MAX_MOTIFS + 1), 0, 0, bytes);
         if (u != MAYURA_OK) {
             free_device(g);
             delete g;

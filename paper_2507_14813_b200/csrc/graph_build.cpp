@@ -82,9 +82,11 @@ static int bits_for(uint64_t maxval) {
 }
 
 // Build one CSR direction: key[e] = vertex owning edge e in this direction, nbr[e] = other end.
+// Each list is followed by a sentinel entry (tr = nbr = 0xFFFFFFFF) so a window scan can stop
+// on "time rank > window end" alone; off[x] = start of list x, off[x+1] - 1 = its sentinel.
 static void build_csr(const std::vector<uint32_t> &key, const std::vector<uint32_t> &nbr,
                       const std::vector<uint32_t> &tr, uint32_t V, int T,
-                      std::vector<uint32_t> &off, std::vector<uint32_t> &ent) {
+                      std::vector<uint32_t> &off, std::vector<uint32_t> &ent, std::vector<uint32_t> &ids_out) {
     const size_t E = key.size();
     std::vector<uint32_t> k(key);
     std::vector<uint32_t> ids(E);
@@ -92,18 +94,58 @@ static void build_csr(const std::vector<uint32_t> &key, const std::vector<uint32
         for (size_t i = lo; i < hi; i++) ids[i] = (uint32_t)i;
     });
     radix_sort_kv(k, ids, bits_for(V ? V - 1 : 0), T);  // stable: ids ascending within a vertex
-    ent.resize(2 * E);
-    parallel_chunks(E, T, [&](size_t lo, size_t hi, int) {
-        for (size_t i = lo; i < hi; i++) {
-            uint32_t e = ids[i];
-            ent[2 * i] = tr[e];
-            ent[2 * i + 1] = nbr[e];
-        }
-    });
     off.assign((size_t)V + 1, 0);
     parallel_chunks((size_t)V + 1, T, [&](size_t lo, size_t hi, int) {
-        for (size_t x = lo; x < hi; x++)
-            off[x] = (uint32_t)(std::lower_bound(k.begin(), k.end(), (uint32_t)x) - k.begin());
+        for (size_t x = lo; x < hi; x++)  // + x: one sentinel slot per earlier list
+            off[x] = (uint32_t)(std::lower_bound(k.begin(), k.end(), (uint32_t)x) - k.begin() + x);
+    });
+    const size_t N = E + V;
+    ent.assign(2 * N, 0xFFFFFFFFu);
+    ids_out.assign(N, 0xFFFFFFFFu);
+    parallel_chunks(E, T, [&](size_t lo, size_t hi, int) {
+        for (size_t i = lo; i < hi; i++) {
+            const uint32_t e = ids[i];
+            const size_t pos = i + k[i];  // sorted position + number of sentinels before it
+            ent[2 * pos] = tr[e];
+            ent[2 * pos + 1] = nbr[e];
+            ids_out[pos] = e;
+        }
+    });
+}
+
+// P(e): first position with time rank > tr[e] in the four lists an edge's endpoints own.
+static void build_succ(mayura_graph_s *g, const std::vector<uint32_t> &out_ids,
+                       const std::vector<uint32_t> &in_ids, int T) {
+    const size_t E = g->E, N = E + g->V;
+    g->eptr.assign(4 * E, 0);
+    auto first_after = [&](const std::vector<uint32_t> &off, const std::vector<uint32_t> &ent, uint32_t x,
+                           uint32_t key) -> uint32_t {
+        uint32_t lo = off[x], hi = off[x + 1] - 1;  // [lo, hi) excludes the sentinel
+        while (lo < hi) {
+            uint32_t mid = lo + (hi - lo) / 2;
+            if (ent[2 * (size_t)mid] > key) hi = mid;
+            else lo = mid + 1;
+        }
+        return lo;
+    };
+    parallel_chunks(E, T, [&](size_t lo, size_t hi, int) {
+        for (size_t e = lo; e < hi; e++) {
+            const uint32_t a = g->src[e], b = g->dst[e], key = g->tr[e];
+            g->eptr[4 * e + 0] = first_after(g->out_off, g->out_ent, a, key);
+            g->eptr[4 * e + 1] = first_after(g->in_off, g->in_ent, b, key);
+            g->eptr[4 * e + 2] = first_after(g->out_off, g->out_ent, b, key);
+            g->eptr[4 * e + 3] = first_after(g->in_off, g->in_ent, a, key);
+        }
+    });
+    g->out_ptr.assign(4 * N, 0);
+    g->in_ptr.assign(4 * N, 0);
+    parallel_chunks(N, T, [&](size_t lo, size_t hi, int) {
+        for (size_t i = lo; i < hi; i++) {
+            if (out_ids[i] != 0xFFFFFFFFu)
+                for (int j = 0; j < 4; j++) g->out_ptr[4 * i + j] = g->eptr[4 * (size_t)out_ids[i] + j];
+            if (in_ids[i] != 0xFFFFFFFFu)
+                for (int j = 0; j < 4; j++) g->in_ptr[4 * i + j] = g->eptr[4 * (size_t)in_ids[i] + j];
+        }
     });
 }
 
@@ -170,8 +212,13 @@ mayura_status build_graph_host(const uint32_t *src, const uint32_t *dst, const i
         }
     });
     // 3. out/in adjacency, each list in increasing edge id (= timestamp) order
-    build_csr(g->src, g->dst, g->tr, V, T, g->out_off, g->out_ent);
-    build_csr(g->dst, g->src, g->tr, V, T, g->in_off, g->in_ent);
+    if (E + (uint64_t)V + 64 > 0xFFFFFFFFull)
+        return fail(MAYURA_E_LIMIT, "mayura_load_graph: n_edges + n_vertices exceeds 32-bit list positions");
+    std::vector<uint32_t> out_ids, in_ids;
+    build_csr(g->src, g->dst, g->tr, V, T, g->out_off, g->out_ent, out_ids);
+    build_csr(g->dst, g->src, g->tr, V, T, g->in_off, g->in_ent, in_ids);
+    // 4. successor pointers
+    build_succ(g, out_ids, in_ids, T);
     return MAYURA_OK;
 }
 

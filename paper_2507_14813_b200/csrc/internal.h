@@ -29,11 +29,21 @@ struct DNode {             // 8 bytes
     uint16_t group_begin;  // groups of this node's children
     uint16_t group_end;
 };
+// Where a group's window starts (DESIGN.md §5 "successor pointers"): P(e) of the edge
+// matched at this node -- slot 0 out(src), 1 in(dst), 2 out(dst), 3 in(src) -- gives
+// the exact first position after t_e; the root edge's R(r) gives a lower bound for
+// lists of motif vertices 0/1 (forward skip); otherwise a lane-cooperative search.
+enum StartKind : uint8_t {
+    START_P0 = 0, START_P1, START_P2, START_P3,  // exact, from the node's own edge
+    START_R0 = 4, START_R1, START_R2, START_R3,  // lower bound, from the root edge
+    START_SEARCH = 8,                           // 32-ary search in the anchor's list
+    START_GLOBAL = 9                            // all edges: search the time-rank array
+};
 struct DGroup {            // 8 bytes
     uint8_t kind;          // AnchorKind
     uint8_t anchor;        // motif vertex whose adjacency is scanned (OUT: u, IN: v)
     uint8_t n_inner;       // children that have children themselves
-    uint8_t pad;
+    uint8_t start;         // StartKind
     uint16_t child_begin;  // contiguous node rows
     uint16_t child_end;
 };
@@ -57,13 +67,19 @@ struct mayura_graph_s {
     std::vector<uint32_t> src, dst, tr;
     std::vector<int64_t> t;
     std::vector<uint64_t> perm;
-    std::vector<uint32_t> out_off, in_off;  // V+1
-    std::vector<uint32_t> out_ent, in_ent;  // 2E: (tr, nbr)
+    std::vector<uint32_t> out_off, in_off;  // V+1; list x = [off[x], off[x+1]-1), sentinel at off[x+1]-1
+    std::vector<uint32_t> out_ent, in_ent;  // 2(E+V): (tr, nbr); sentinel = (0xFFFFFFFF, 0xFFFFFFFF)
+    std::vector<uint32_t> eptr;             // 4E: P(e) = first list position with time > t_e in
+                                            //     out(src e), in(dst e), out(dst e), in(src e)
+    std::vector<uint32_t> out_ptr, in_ptr;  // 4(E+V): P(e) of each list entry's edge (sentinel: 0)
     // device arrays
     uint32_t *d_src = nullptr, *d_dst = nullptr, *d_tr = nullptr, *d_hi = nullptr;
     int64_t *d_t = nullptr;
     uint32_t *d_out_off = nullptr, *d_in_off = nullptr;
     uint32_t *d_out_ent = nullptr, *d_in_ent = nullptr;  // uint2 {tr, nbr}
+    uint32_t *d_eptr = nullptr, *d_out_ptr = nullptr, *d_in_ptr = nullptr;  // uint4
+    uint32_t *d_ctx = nullptr;                            // offloaded search contexts
+    uint32_t ctx_cap = 0, epoch = 0;
     uint32_t *d_queue = nullptr;                         // work-queue cursors
     unsigned long long *d_counts = nullptr;              // scratch counts (host-output calls)
     uint32_t d_counts_cap = 0;

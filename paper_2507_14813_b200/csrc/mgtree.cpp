@@ -126,6 +126,15 @@ mayura_status flatten(const std::vector<TrieNode> &trie, uint32_t n_motifs_total
             DGroup dg{};
             dg.kind = (uint8_t)g.first.first;
             dg.anchor = (uint8_t)g.first.second;
+            // window start source: the node's own edge (x.u -> x.v) gives exact successor
+            // pointers for its endpoints; the root edge (0 -> 1) a lower bound for 0 and 1.
+            if (dg.kind == ANCHOR_GLOBAL) dg.start = START_GLOBAL;
+            else if (dg.kind == ANCHOR_OUT)
+                dg.start = dg.anchor == x.u ? START_P0 : dg.anchor == x.v ? START_P2
+                         : dg.anchor == 0 ? START_R0 : dg.anchor == 1 ? START_R2 : START_SEARCH;
+            else
+                dg.start = dg.anchor == x.v ? START_P1 : dg.anchor == x.u ? START_P3
+                         : dg.anchor == 1 ? START_R1 : dg.anchor == 0 ? START_R3 : START_SEARCH;
             dg.child_begin = (uint16_t)trie_of.size();
             uint32_t inner = 0;
             for (int c : g.second) {

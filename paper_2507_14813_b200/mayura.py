@@ -34,6 +34,7 @@ SIGNATURES = {
     "mayura_load_graph": ([_P, _P, _P, _u64, _u32, _int, _PP], _int),
     "mayura_graph_info": ([_P, _P, _P, _P], _int),
     "mayura_graph_export": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _int),
+    "mayura_graph_export_succ": ([_P, _P], _int),
     "mayura_free_graph": ([_P], None),
     "mayura_build_mgtree": ([_P, _P, _u32, _i64, _PP], _int),
     "mayura_mgtree_info": ([_P, _P, _P, _P, _P, _P, _P], _int),
@@ -54,7 +55,8 @@ for _name, (_args, _res) in SIGNATURES.items():
 
 STATUS = {0: "MAYURA_OK", -1: "MAYURA_E_INVALID", -2: "MAYURA_E_LIMIT", -3: "MAYURA_E_OOM",
           -4: "MAYURA_E_CUDA", -5: "MAYURA_E_STATE"}
-STATS_FIELDS = ("roots", "nodes", "windows", "entries", "probes", "batches", "bytes_alg", "matches")
+STATS_FIELDS = ("roots", "nodes", "windows", "entries", "probes", "batches", "bytes_alg", "matches",
+                "offloads", "contexts")
 
 
 class MayuraError(RuntimeError):
@@ -105,11 +107,18 @@ def mayura_graph_export(g: int) -> dict:
     E, V, _ = mayura_graph_info(g)
     out = dict(src=np.empty(E, np.uint32), dst=np.empty(E, np.uint32), t=np.empty(E, np.int64),
                tr=np.empty(E, np.uint32), perm=np.empty(E, np.uint64),
-               out_off=np.empty(V + 1, np.uint32), out_ent=np.empty(2 * E, np.uint32),
-               in_off=np.empty(V + 1, np.uint32), in_ent=np.empty(2 * E, np.uint32))
+               out_off=np.empty(V + 1, np.uint32), out_ent=np.empty(2 * (E + V), np.uint32),
+               in_off=np.empty(V + 1, np.uint32), in_ent=np.empty(2 * (E + V), np.uint32))
     _check(_lib.mayura_graph_export(g, *[_ptr(out[k]) for k in ("src", "dst", "t", "tr", "perm", "out_off",
                                                                  "out_ent", "in_off", "in_ent")]))
     return out
+
+
+def mayura_graph_export_succ(g: int) -> np.ndarray:
+    E, _, _ = mayura_graph_info(g)
+    out = np.empty(4 * E, np.uint32)
+    _check(_lib.mayura_graph_export_succ(g, _ptr(out)))
+    return out.reshape(E, 4)
 
 
 def mayura_free_graph(g: int) -> None:
@@ -203,7 +212,9 @@ class Graph:
         self.n_edges, self.n_vertices, self.device_bytes = mayura_graph_info(self.handle)
 
     def export(self) -> dict:
-        return mayura_graph_export(self.handle)
+        d = mayura_graph_export(self.handle)
+        d["eptr"] = mayura_graph_export_succ(self.handle)
+        return d
 
     def partition(self, delta: int, n_parts: int) -> List[int]:
         return mayura_partition_roots(self.handle, delta, n_parts)

@@ -42,13 +42,23 @@ def test_host_graph_builder_matches_definition(M):
     ts = t[order]
     assert np.array_equal(ex["t"], ts)
     assert np.array_equal(ex["tr"], np.searchsorted(ts, ts, side="left"))
+    lists = {}
     for direction, key, nbr in (("out", ex["src"], ex["dst"]), ("in", ex["dst"], ex["src"])):
         off, ent = ex[direction + "_off"], ex[direction + "_ent"].reshape(-1, 2)
-        assert off[0] == 0 and off[-1] == len(src)
+        assert off[0] == 0 and off[-1] == len(src) + V
         for x in range(V):
             ids = np.nonzero(key == x)[0]       # edge ids of x, increasing = time order
-            sl = ent[off[x]:off[x + 1]]
+            sl = ent[off[x]:off[x + 1] - 1]
             assert np.array_equal(sl[:, 0], ex["tr"][ids]) and np.array_equal(sl[:, 1], nbr[ids])
+            assert tuple(ent[off[x + 1] - 1]) == (0xFFFFFFFF, 0xFFFFFFFF)   # sentinel
+        lists[direction] = (off, ent)
+    # successor pointers: first position after t_e in out(a), in(b), out(b), in(a)
+    for e in range(0, len(src), 7):
+        a, b, tre = ex["src"][e], ex["dst"][e], ex["tr"][e]
+        for j, (d, x) in enumerate((("out", a), ("in", b), ("out", b), ("in", a))):
+            off, ent = lists[d]
+            seg = ent[off[x]:off[x + 1] - 1, 0]
+            assert ex["eptr"][e, j] == off[x] + np.searchsorted(seg, tre, side="right")
     g.close()
 
 

@@ -189,3 +189,22 @@ def test_stats_kernel_counts_and_work(M):
     assert st["matches"] == sum(M.comine(g, tree))
     assert st["roots"] == int((src != dst).sum())
     assert st["entries"] < si["entries"] and st["bytes_alg"] < si["bytes_alg"]  # co-mining removes work
+
+
+def test_heavy_hub_roots_offload(M):
+    """One hub with a dense burst: per-root search trees of 10^5-10^6 nodes.  The dynamic
+    context offload (idle warps) must split them and counts must stay exact."""
+    n, delta = 4000, 1000
+    src, dst, t, V = synth.out_star(n)
+    g = M.Graph(src, dst, t, V, device=0)
+    tree = M.MGTree([synth.MOTIFS["star_out3"], [(0, 1), (0, 2)]], delta)
+    assert M.comine(g, tree) == [_pins.star_fanout_count(n, 3, delta), _pins.star_fanout_count(n, 2, delta)]
+    st = M.comine_stats(g, tree)
+    assert st["offloads"] > 0 and st["contexts"] > 0
+    assert st["matches"] == _pins.star_fanout_count(n, 3, delta) + _pins.star_fanout_count(n, 2, delta)
+    # mixed: the hub burst plus random background, vs the oracle
+    import oracle
+    s2, d2, t2, V2 = synth.random_graph(5, 50, 20_000, 20_000)
+    src = np.concatenate([src, s2 + V]); dst = np.concatenate([dst, d2 + V]); t = np.concatenate([t, t2])
+    motifs = synth.group(synth.GROUP_C2)
+    assert gpu_counts(M, src, dst, t, V + V2, motifs, 300) == oracle.backtrack(src, dst, t, V + V2, motifs, 300)

@@ -48,6 +48,7 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr int kCtxWords = 32;               // one context = 128 bytes
 constexpr uint32_t kCtxCap = 1u << 20;      // contexts per launch (128 MiB)
+constexpr uint32_t kSmallRows = 64;         // trees up to this many rows/groups: table in parameter space
 enum { S_GROUP = 0, S_BATCH = 1, S_ITER = 2 };
 enum { ST_ROOTS, ST_NODES, ST_WINDOWS, ST_ENTRIES, ST_PROBES, ST_BATCHES, ST_BYTES, ST_MATCHES,
        ST_OFFLOADS, ST_CONTEXTS, ST_N };
@@ -70,6 +71,8 @@ struct KParams {
     uint32_t ctx_cap, epoch;
     unsigned long long *counts;
     unsigned long long *stats;
+    DNode tn[kSmallRows];   // small trees: the table itself (parameter space)
+    DGroup tg[kSmallRows];
 };
 
 struct __align__(16) Frame {  // one per warp per DFS depth (shared memory), 3 x 16 bytes
@@ -190,20 +193,27 @@ __device__ __forceinline__ uint32_t locate(bool global, const uint2 *__restrict_
     return lo;
 }
 
+// CNT > 0 ("small" trees, <= 64 rows and groups): the table lives in the kernel's parameter
+// space (constant bank; warp-uniform indexed loads) and the counters in lane registers.
+// CNT == 0: table and counters in dynamic shared memory.
 template <int MAXV, int CNT, bool STATS>
-__global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
+__global__ void __launch_bounds__(kBlock, 4) comine_kernel(const __grid_constant__ KParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    Frame *s_frames = reinterpret_cast<Frame *>(smem);
-    unsigned long long *s_cnt = reinterpret_cast<unsigned long long *>(s_frames + kWarps * kMaxDepth);
-    DNode *s_nodes = reinterpret_cast<DNode *>(s_cnt + p.n_nodes);
+    __shared__ Frame s_frames[kWarps * kMaxDepth];
+    __shared__ uint32_t s_masks[kWarps * kMaxDepth * kMaxGroupChildren];
+    __shared__ unsigned long long s_cnt_small[CNT > 0 ? kSmallRows : 1];
+    unsigned long long *s_cnt = CNT > 0 ? s_cnt_small : reinterpret_cast<unsigned long long *>(smem);
+    DNode *s_nodes = reinterpret_cast<DNode *>(reinterpret_cast<unsigned long long *>(smem) + p.n_nodes);
     DGroup *s_groups = reinterpret_cast<DGroup *>(s_nodes + p.n_nodes);
-    uint32_t *s_masks = reinterpret_cast<uint32_t *>(s_groups + p.n_groups);
+#define NODE(i) (CNT > 0 ? p.tn[(i)] : s_nodes[(i)])
+#define GROUP(i) (CNT > 0 ? p.tg[(i)] : s_groups[(i)])
 
     for (uint32_t i = threadIdx.x; i < p.n_nodes; i += blockDim.x) {
-        s_nodes[i] = p.nodes[i];
+        if (CNT == 0) s_nodes[i] = p.nodes[i];
         s_cnt[i] = 0;
     }
-    for (uint32_t i = threadIdx.x; i < p.n_groups; i += blockDim.x) s_groups[i] = p.groups[i];
+    if (CNT == 0)
+        for (uint32_t i = threadIdx.x; i < p.n_groups; i += blockDim.x) s_groups[i] = p.groups[i];
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
         if (STATS && lane == 0) st[ST_MATCHES] += __popc(m);
     };
 
-    const DNode root = s_nodes[0];
+    const DNode root = NODE(0);
     bool roots_done = false, idle = false;
     uint32_t ticket = kNone;  // lane 0: claimed queue slot not yet published
 
@@ -276,7 +286,8 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
                         ex = 1;
                         break;
                     }
-                    __nanosleep(spin < 4 ? 32 : 200);
+                    // exponential backoff: waiting warps must not steal issue slots from working ones
+                    __nanosleep(64u << (spin < 5 ? spin : 5));
                 }
                 if (got != kNone) {
                     atomicSub(p.lb + LB_IDLE, 1u);
@@ -393,14 +404,14 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
                                __shfl_sync(kFull, w, 12));
 #pragma unroll
                 for (int k = 0; k < MAXV; k++) m2g[k] = __shfl_sync(kFull, w, 13 + k);
-                const DNode dn = s_nodes[node];
+                const DNode dn = NODE(node);
                 nv = dn.nv;
                 g_end = (lim != kNone) ? g + 1 : dn.group_end;
                 depth = 0;
                 if (pos == kNone) {
                     state = S_GROUP;
                 } else {
-                    kind = s_groups[g].kind;
+                    kind = GROUP(g).kind;
                     nbatch = 1;  // a continuation: may split again
                     state = S_BATCH;
                 }
@@ -417,8 +428,8 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
                         const Frame f = F[depth];
                         node = f.node_g & 0xffffu; g = f.node_g >> 16; ci = f.ci; tr_prev = f.tr_prev;
                         pos = f.pos; batch = f.batch; mask = f.mask; lim = f.lim; g_end = f.g_end; P = f.P;
-                        const DGroup G = s_groups[g];
-                        nv = s_nodes[node].nv;
+                        const DGroup G = GROUP(g);
+                        nv = NODE(node).nv;
                         kind = G.kind; c_end = G.child_end;
                         const uint32_t idx = batch + lane;
                         if (kind == ANCHOR_GLOBAL) {
@@ -431,7 +442,7 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
                         }
                         state = S_ITER;
                     } else {
-                        const DGroup G = s_groups[g];
+                        const DGroup G = GROUP(g);
                         kind = G.kind;
                         nbatch = 0;
                         if (G.start < START_R0) {
@@ -456,7 +467,7 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
                     }
                 }
                 if (state == S_BATCH) {
-                    const DGroup G = s_groups[g];
+                    const DGroup G = GROUP(g);
                     if (pos >= lim) {
                         ++g;
                         state = S_GROUP;
@@ -567,7 +578,7 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
                         cls = classify<MAXV>(m2g, nv, e1);
                     bool any_inner = false;
                     for (uint32_t c = G.child_begin; c < G.child_end; ++c) {
-                        const DNode dn = s_nodes[c];
+                        const DNode dn = NODE(c);
                         const unsigned mc = __ballot_sync(kFull, w && cls == dn.want);
                         if (dn.flags & NODE_COMPLETION) count(c, mc);
                         if (dn.flags & NODE_INNER) {
@@ -579,14 +590,14 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
                     __syncwarp();
                     ci = G.child_begin;
                     c_end = G.child_end;
-                    mask = (s_nodes[ci].flags & NODE_INNER) ? MS[depth * kMaxGroupChildren] : 0u;
+                    mask = (NODE(ci).flags & NODE_INNER) ? MS[depth * kMaxGroupChildren] : 0u;
                     state = S_ITER;
                 }
                 // ---- S_ITER: next (inner child, candidate) pair of the current batch
                 while (mask == 0) {
                     if (++ci >= c_end) break;
-                    const uint32_t cb = s_groups[g].child_begin;
-                    mask = (s_nodes[ci].flags & NODE_INNER) ? MS[depth * kMaxGroupChildren + (ci - cb)] : 0u;
+                    const uint32_t cb = GROUP(g).child_begin;
+                    mask = (NODE(ci).flags & NODE_INNER) ? MS[depth * kMaxGroupChildren + (ci - cb)] : 0u;
                 }
                 if (mask == 0) {
                     state = S_BATCH;
@@ -604,7 +615,7 @@ __global__ void __launch_bounds__(kBlock) comine_kernel(KParams p) {
                     f.batch = batch; f.mask = mask; f.lim = lim; f.g_end = g_end; f.P = P;
                     F[depth] = f;
                 }
-                const DNode dc = s_nodes[ci];
+                const DNode dc = NODE(ci);
                 if (dc.n_new >= 1) m2g_set<MAXV>(m2g, nv, c1);
                 if (dc.n_new == 2) m2g_set<MAXV>(m2g, nv + 1, c2);
                 nv = dc.nv;
@@ -682,10 +693,13 @@ struct DeviceTable {
     uint32_t n_nodes, n_groups, n_motifs, max_vertices;
 };
 
+bool small_table(uint32_t n_nodes, uint32_t n_groups) { return n_nodes <= kSmallRows && n_groups <= kSmallRows; }
+
+// dynamic shared memory: only large trees keep their counters, rows and groups there
 size_t smem_bytes(uint32_t n_nodes, uint32_t n_groups) {
-    return sizeof(Frame) * kWarps * kMaxDepth + (size_t)n_nodes * sizeof(unsigned long long) +
-           (size_t)n_nodes * sizeof(DNode) + (size_t)n_groups * sizeof(DGroup) +
-           sizeof(uint32_t) * kWarps * kMaxDepth * kMaxGroupChildren;
+    if (small_table(n_nodes, n_groups)) return 0;
+    return (size_t)n_nodes * sizeof(unsigned long long) + (size_t)n_nodes * sizeof(DNode) +
+           (size_t)n_groups * sizeof(DGroup);
 }
 
 mayura_status cuda_fail(cudaError_t e, const char *what) {
@@ -733,15 +747,17 @@ cudaError_t launch_comine_t(const KParams &p, size_t smem, cudaStream_t s, int s
 template <int MAXV>
 cudaError_t launch_comine_v(const KParams &p, bool stats, cudaStream_t s, int sms) {
     const size_t smem = smem_bytes(p.n_nodes, p.n_groups);
-    if (p.n_nodes <= 32)
+    const bool small = small_table(p.n_nodes, p.n_groups);
+    if (small && p.n_nodes <= 32)
         return stats ? launch_comine_t<MAXV, 1, true>(p, smem, s, sms) : launch_comine_t<MAXV, 1, false>(p, smem, s, sms);
-    if (p.n_nodes <= 64)
+    if (small)
         return stats ? launch_comine_t<MAXV, 2, true>(p, smem, s, sms) : launch_comine_t<MAXV, 2, false>(p, smem, s, sms);
     return stats ? launch_comine_t<MAXV, 0, true>(p, smem, s, sms) : launch_comine_t<MAXV, 0, false>(p, smem, s, sms);
 }
 
 cudaError_t launch_comine(const KParams &p, uint32_t max_vertices, bool stats, cudaStream_t s, int sms) {
     if (max_vertices <= 4) return launch_comine_v<4>(p, stats, s, sms);
+    if (max_vertices <= 6) return launch_comine_v<6>(p, stats, s, sms);
     if (max_vertices <= 8) return launch_comine_v<8>(p, stats, s, sms);
     return launch_comine_v<16>(p, stats, s, sms);
 }
@@ -889,6 +905,13 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
             p.in_ptr = reinterpret_cast<const uint4 *>(g->d_in_ptr);
             p.nodes = dt.nodes; p.groups = dt.groups; p.motif_node = dt.motif_node;
             p.n_nodes = dt.n_nodes; p.n_groups = dt.n_groups; p.n_motifs = dt.n_motifs;
+            std::memset(p.tn, 0, sizeof(p.tn));
+            std::memset(p.tg, 0, sizeof(p.tg));
+            if (small_table(dt.n_nodes, dt.n_groups)) {
+                const Table &ht = mode == 1 ? m->single[i] : m->group;
+                std::memcpy(p.tn, ht.nodes.data(), sizeof(DNode) * ht.nodes.size());
+                std::memcpy(p.tg, ht.groups.data(), sizeof(DGroup) * ht.groups.size());
+            }
             p.r0 = (uint32_t)rb; p.n_roots = n_roots;
             p.lb = g->d_queue + LB_N * i;
             p.ctx = g->d_ctx;

@@ -49,6 +49,7 @@ constexpr uint32_t kNone = 0xffffffffu;
 constexpr int kCtxWords = 32;               // one context = 128 bytes
 constexpr uint32_t kCtxCap = 1u << 20;      // contexts per launch (128 MiB)
 constexpr uint32_t kSmallRows = 64;         // trees up to this many rows/groups: table in parameter space
+constexpr uint32_t kSweepMax = 32;          // leaf sweep: longest per-lane window
 enum { S_GROUP = 0, S_BATCH = 1, S_ITER = 2 };
 enum { ST_ROOTS, ST_NODES, ST_WINDOWS, ST_ENTRIES, ST_PROBES, ST_BATCHES, ST_BYTES, ST_MATCHES,
        ST_OFFLOADS, ST_CONTEXTS, ST_N };
@@ -227,15 +228,16 @@ __global__ void __launch_bounds__(kBlock, 4) comine_kernel(const __grid_constant
     for (int i = 0; i < ST_N; i++) st[i] = 0;
 
     // counter of trie node c (warp-uniform c, m): lane c%32 owns it (CNT > 0) or shared memory
-    auto count = [&](uint32_t c, unsigned m) {
+    // add n (warp-uniform) matches to trie node c's counter
+    auto count = [&](uint32_t c, uint32_t n) {
         if (CNT == 0) {
-            if (lane == 0 && m) atomicAdd(&s_cnt[c], (unsigned long long)__popc(m));
+            if (lane == 0 && n) atomicAdd(&s_cnt[c], (unsigned long long)n);
         } else {
 #pragma unroll
             for (int s = 0; s < (CNT > 0 ? CNT : 1); s++)
-                if (c == (uint32_t)(lane + 32 * s)) cnt[s] += __popc(m);
+                if (c == (uint32_t)(lane + 32 * s)) cnt[s] += n;
         }
-        if (STATS && lane == 0) st[ST_MATCHES] += __popc(m);
+        if (STATS && lane == 0) st[ST_MATCHES] += n;
     };
 
     const DNode root = NODE(0);
@@ -253,17 +255,27 @@ __global__ void __launch_bounds__(kBlock, 4) comine_kernel(const __grid_constant
 
     for (;;) {
         // ------------------------------------------------------- acquire work
-        uint32_t chunk_base = kNone, ctx_slot = kNone;
+        uint32_t chunk_base = kNone, chunk_len = 0, ctx_slot = kNone;
         bool quit = false;
         if (!roots_done) {
-            uint32_t b = 0;
+            // guided self-scheduling: chunks shrink from 32 roots to 1 as the queue drains,
+            // so the root queue lasts until the end of the launch
+            uint32_t b = 0, sz = 0;
             if (lane == 0) {
-                b = atomicAdd(p.lb + LB_ROOT, 32u);
+                const uint32_t cur = ld_relaxed(p.lb + LB_ROOT);
+                const uint32_t rem = cur < p.n_roots ? p.n_roots - cur : 0u;
+                sz = max(1u, min(32u, rem / (2u * gridDim.x * kWarps)));
+                b = atomicAdd(p.lb + LB_ROOT, sz);
                 if (b < p.n_roots) atomicAdd(p.lb + LB_WORK, 1u);
             }
             b = __shfl_sync(kFull, b, 0);
-            if (b < p.n_roots) chunk_base = b;
-            else roots_done = true;
+            sz = __shfl_sync(kFull, sz, 0);
+            if (b < p.n_roots) {
+                chunk_base = b;
+                chunk_len = min(sz, p.n_roots - b);
+            } else {
+                roots_done = true;
+            }
         }
         if (chunk_base == kNone) {
             // context phase: take a ticket (queue slot) and wait for it to be published, or exit
@@ -307,7 +319,7 @@ __global__ void __launch_bounds__(kBlock, 4) comine_kernel(const __grid_constant
         uint4 rp = make_uint4(0, 0, 0, 0);
         unsigned pending = 0;
         if (chunk_base != kNone) {
-            const bool valid = chunk_base + lane < p.n_roots;
+            const bool valid = (uint32_t)lane < chunk_len;
             const uint32_t r = p.r0 + chunk_base + lane;
             if (valid) {
                 rs = __ldg(p.src + r);
@@ -324,7 +336,7 @@ __global__ void __launch_bounds__(kBlock, 4) comine_kernel(const __grid_constant
                     st[ST_BYTES] += 16ull * __popc(vm) + ((root.flags & NODE_INNER) ? 16ull * __popc(pending) : 0);
                 }
             }
-            if (root.flags & NODE_COMPLETION) count(0, pending);
+            if (root.flags & NODE_COMPLETION) count(0, __popc(pending));
             if (!(root.flags & NODE_INNER)) pending = 0;
         }
 
@@ -579,8 +591,74 @@ __global__ void __launch_bounds__(kBlock, 4) comine_kernel(const __grid_constant
                     bool any_inner = false;
                     for (uint32_t c = G.child_begin; c < G.child_end; ++c) {
                         const DNode dn = NODE(c);
-                        const unsigned mc = __ballot_sync(kFull, w && cls == dn.want);
-                        if (dn.flags & NODE_COMPLETION) count(c, mc);
+                        unsigned mc = __ballot_sync(kFull, w && cls == dn.want);
+                        if (dn.flags & NODE_COMPLETION) count(c, __popc(mc));
+                        if ((dn.flags & NODE_SWEEP) && mc) {
+                            // ---- leaf sweep: child c's subtree is one level of completions; each
+                            // lane takes one candidate and scans its (short) windows itself
+                            bool act = (mc >> lane) & 1u;
+                            // windows of >= kSweepMax entries go to the warp path (descent)
+                            for (uint32_t g2 = dn.group_begin; g2 < dn.group_end; ++g2) {
+                                const DGroup G2 = GROUP(g2);
+                                const uint32_t s0 = G2.start < START_R0 ? pick(ep, G2.start)
+                                                                        : pick(R, G2.start - START_R0);
+                                const uint2 *ent2 = G2.kind == ANCHOR_OUT ? p.out_ent : p.in_ent;
+                                if (act && __ldg(&ent2[s0 + kSweepMax].x) <= h) act = false;
+                            }
+                            const unsigned fb = __ballot_sync(kFull, ((mc >> lane) & 1u) && !act);
+                            if (fb != mc) {
+                                const uint32_t xa = e1, xb = e2, tl = etr;  // the candidate edge
+                                for (uint32_t g2 = dn.group_begin; g2 < dn.group_end; ++g2) {
+                                    const DGroup G2 = GROUP(g2);
+                                    uint32_t s0 = G2.start < START_R0 ? pick(ep, G2.start)
+                                                                      : pick(R, G2.start - START_R0);
+                                    const uint2 *ent2 = G2.kind == ANCHOR_OUT ? p.out_ent : p.in_ent;
+                                    const uint32_t nch = G2.child_end - G2.child_begin;
+                                    const uint32_t w0 = NODE(G2.child_begin).want;
+                                    const uint32_t w1 = nch > 1 ? NODE(G2.child_begin + 1).want : 0xFDu;
+                                    const uint32_t w2 = nch > 2 ? NODE(G2.child_begin + 2).want : 0xFDu;
+                                    const uint32_t w3 = nch > 3 ? NODE(G2.child_begin + 3).want : 0xFDu;
+                                    uint32_t n0 = 0, n1 = 0, n2 = 0, n3 = 0, ne = 0;
+                                    bool go = act;
+                                    while (__any_sync(kFull, go)) {
+                                        if (go) {
+                                            const uint2 e = __ldg(ent2 + s0);
+                                            if (e.x > h) {
+                                                go = false;
+                                            } else {
+                                                if (e.x > tl) {
+                                                    const uint32_t cl =
+                                                        (dn.n_new >= 1 && e.y == xa) ? nv
+                                                        : (dn.n_new == 2 && e.y == xb) ? nv + 1
+                                                        : classify<MAXV>(m2g, nv, e.y);
+                                                    n0 += cl == w0;
+                                                    n1 += cl == w1;
+                                                    n2 += cl == w2;
+                                                    n3 += cl == w3;
+                                                    ++ne;
+                                                }
+                                                ++s0;
+                                            }
+                                        }
+                                    }
+                                    count(G2.child_begin, __reduce_add_sync(kFull, n0));
+                                    if (nch > 1) count(G2.child_begin + 1, __reduce_add_sync(kFull, n1));
+                                    if (nch > 2) count(G2.child_begin + 2, __reduce_add_sync(kFull, n2));
+                                    if (nch > 3) count(G2.child_begin + 3, __reduce_add_sync(kFull, n3));
+                                    if (STATS) {
+                                        const uint32_t te = __reduce_add_sync(kFull, ne);
+                                        const uint32_t tw = __popc(__ballot_sync(kFull, act));
+                                        if (lane == 0) {
+                                            st[ST_WINDOWS] += tw;
+                                            st[ST_ENTRIES] += te;
+                                            st[ST_BYTES] += 8ull * (te + tw);
+                                        }
+                                    }
+                                }
+                                if (STATS && lane == 0) st[ST_NODES] += __popc(mc & ~fb);
+                            }
+                            mc = fb;
+                        }
                         if (dn.flags & NODE_INNER) {
                             if (lane == 0) MS[depth * kMaxGroupChildren + (c - G.child_begin)] = mc;
                             any_inner |= (mc != 0);
@@ -1008,8 +1086,9 @@ extern "C" mayura_status mayura_load_graph(const uint32_t *src, const uint32_t *
         if (u == MAYURA_OK) u = up(g->d_eptr, g->eptr, 0, 4 * PADE, 0, bytes);
         if (u == MAYURA_OK) u = up(g->d_out_off, g->out_off, 0, 0, 0, bytes);
         if (u == MAYURA_OK) u = up(g->d_in_off, g->in_off, 0, 0, 0, bytes);
-        if (u == MAYURA_OK) u = up(g->d_out_ent, g->out_ent, 0, 2 * PADE, 0xFF, bytes);  // sentinel padding
-        if (u == MAYURA_OK) u = up(g->d_in_ent, g->in_ent, 0, 2 * PADE, 0xFF, bytes);
+        // sentinel padding: a batch (32) or a leaf-sweep length probe (kSweepMax) never reads past it
+        if (u == MAYURA_OK) u = up(g->d_out_ent, g->out_ent, 0, 2 * (PADE + kSweepMax), 0xFF, bytes);
+        if (u == MAYURA_OK) u = up(g->d_in_ent, g->in_ent, 0, 2 * (PADE + kSweepMax), 0xFF, bytes);
         if (u == MAYURA_OK) u = up(g->d_out_ptr, g->out_ptr, 0, 4 * PADE, 0, bytes);
         if (u == MAYURA_OK) u = up(g->d_in_ptr, g->in_ptr, 0, 4 * PADE, 0, bytes);
         if (u == MAYURA_OK) u = up(g->d_queue, none, (size_t)LB_N * (MAYURA_MAX_MOTIFS + 1), 0, 0, bytes);

@@ -47,7 +47,11 @@ struct DGroup {            // 8 bytes
     uint16_t child_begin;  // contiguous node rows
     uint16_t child_end;
 };
-static constexpr uint8_t NODE_COMPLETION = 1, NODE_INNER = 2;
+// NODE_SWEEP: every child group of the node is an OUT/IN list group whose window start comes
+// from successor pointers (START_P*/START_R*), holds <= kSweepChildren children, all leaves --
+// the kernel counts such a node's subtree for 32 candidates at once, one lane per candidate.
+static constexpr uint8_t NODE_COMPLETION = 1, NODE_INNER = 2, NODE_SWEEP = 4;
+static constexpr uint32_t kSweepChildren = 4;
 
 struct Table {
     std::vector<DNode> nodes;          // row 0 = root (canonical edge 0->1)

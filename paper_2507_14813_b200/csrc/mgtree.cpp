@@ -162,6 +162,13 @@ mayura_status flatten(const std::vector<TrieNode> &trie, uint32_t n_motifs_total
         // dx may be invalidated by push_back: re-index
         tab.nodes[q].group_begin = (uint16_t)gb;
         tab.nodes[q].group_end = (uint16_t)tab.groups.size();
+        bool sweep = !x.children.empty();
+        for (uint32_t gi = gb; gi < tab.groups.size(); gi++) {
+            const DGroup &dg = tab.groups[gi];
+            sweep = sweep && dg.kind != ANCHOR_GLOBAL && dg.start < START_SEARCH && dg.n_inner == 0 &&
+                    (uint32_t)(dg.child_end - dg.child_begin) <= kSweepChildren;
+        }
+        if (sweep) tab.nodes[q].flags |= NODE_SWEEP;
     }
     return MAYURA_OK;
 }

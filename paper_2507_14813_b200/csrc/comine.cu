@@ -287,14 +287,17 @@ __global__ void __launch_bounds__(kBlock, 4) comine_kernel(const __grid_constant
                     idle = true;
                 }
                 if (ticket == kNone) ticket = atomicAdd(p.lb + LB_HEAD, 1u);
+                // polls are relaxed loads: a gpu-scope acquire would invalidate this SM's L1
+                // (CCTL.IVALL) on every poll; one fence follows a successful poll instead
                 for (int spin = 0;; spin++) {
                     if (ticket < p.ctx_cap &&
-                        ld_acquire(p.ctx + (size_t)ticket * kCtxWords + (kCtxWords - 1)) == p.epoch) {
+                        ld_relaxed(p.ctx + (size_t)ticket * kCtxWords + (kCtxWords - 1)) == p.epoch) {
                         got = ticket;
                         ticket = kNone;
+                        __threadfence();
                         break;
                     }
-                    if (ld_acquire(p.lb + LB_WORK) == 0) {
+                    if (ld_relaxed(p.lb + LB_WORK) == 0) {
                         ex = 1;
                         break;
                     }
@@ -393,10 +396,7 @@ __global__ void __launch_bounds__(kBlock, 4) comine_kernel(const __grid_constant
                 if (ctx_slot == kNone) break;
                 uint32_t w = 0;
                 if (ctx_slot < p.ctx_cap) {
-                    if (lane == 0)
-                        while (ld_acquire(p.ctx + (size_t)ctx_slot * kCtxWords + (kCtxWords - 1)) != p.epoch)
-                            __nanosleep(32);
-                    __syncwarp();
+                    __syncwarp();  // lane 0 observed the flag and fenced
                     w = __ldcg(p.ctx + (size_t)ctx_slot * kCtxWords + lane);
                 } else {
                     w = kNone;

@@ -221,8 +221,8 @@ def main():
     g = M.Graph(src, dst, t, V, device=local)
     tree = M.MGTree(cfg.group(), cfg.delta)
     k = tree.n_motifs
-    bounds = g.partition(cfg.delta, world)
-    rb, re_ = bounds[rank], bounds[rank + 1]
+    from paper_2507_14813_b200 import parallel
+    rb, re_ = parallel.shard_range(g, cfg.delta, rank, world)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
     counts = torch.zeros(k, dtype=torch.int64, device=dev)
@@ -239,8 +239,7 @@ def main():
         for i in range(warmup):
             flush.fill_(i)
             M.mayura_comine_ex(g.handle, tree.handle, rb, re_, sp, counts, independent, ev[0][1].cuda_event)
-            if world > 1:
-                dist.all_reduce(counts)
+            parallel.reduce_counts(counts)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -251,8 +250,7 @@ def main():
             e0.record(stream)
             M.mayura_comine_ex(g.handle, tree.handle, rb, re_, sp, counts, independent, em.cuda_event)
             ek.record(stream)
-            if world > 1:
-                dist.all_reduce(counts)
+            parallel.reduce_counts(counts)
             e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -311,10 +309,8 @@ def main():
             t0 = time.perf_counter()
             g2 = M.Graph(pin_src, pin_dst, pin_t, V, device=local)   # host build + H2D
             if world > 1:
-                b2 = g2.partition(cfg.delta, world)
                 c2 = torch.zeros(k, dtype=torch.int64, device=dev)
-                M.mayura_comine(g2.handle, tree.handle, b2[rank], b2[rank + 1], sp, c2)
-                dist.all_reduce(c2)
+                parallel.comine_distributed(g2, tree, c2, sp)
                 host_counts = c2.cpu().tolist()                          # D2H
             else:
                 host_counts = M.comine(g2, tree)                         # kernels + D2H

@@ -31,6 +31,8 @@
 // All arithmetic is integer (u32 ids and time ranks, i64 timestamps, u64 counts).
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -54,7 +56,7 @@ enum { S_GROUP = 0, S_BATCH = 1, S_ITER = 2 };
 enum { ST_ROOTS, ST_NODES, ST_WINDOWS, ST_ENTRIES, ST_PROBES, ST_BATCHES, ST_BYTES, ST_MATCHES,
        ST_OFFLOADS, ST_CONTEXTS, ST_N };
 // load-balancer words (zeroed by window_end_kernel)
-enum { LB_ROOT = 0, LB_TAIL = 1, LB_HEAD = 2, LB_IDLE = 3, LB_WORK = 4, LB_N = 8 };
+enum { LB_ROOT = 0, LB_TAIL = 1, LB_HEAD = 2, LB_IDLE = 3, LB_WORK = 4, LB_ERR = 5, LB_N = 8 };
 
 struct KParams {
     const uint32_t *src, *dst, *tr, *hi;
@@ -731,6 +733,11 @@ __global__ void __launch_bounds__(kBlock, 4) comine_kernel(const __grid_constant
     }
 }
 
+#include "lane.cuh"
+#include "bfs.cuh"
+#include "wave.cuh"
+#include "tile.cuh"
+
 // a2: hi[r] = (last edge id e with t[e] <= t[r] + delta), by galloping from r (windows
 // are short) then binary search.  Also zeroes the load-balancer words and the output
 // counts of this call, so a co-mining query is exactly two launches.
@@ -768,8 +775,46 @@ struct DeviceTable {
     DNode *nodes;
     DGroup *groups;
     uint32_t *motif_node;
-    uint32_t n_nodes, n_groups, n_motifs, max_vertices;
+    lane::LNode *lnodes;
+    uint32_t *gwant;
+    uint32_t n_nodes, n_groups, n_motifs, max_vertices, max_edges, n_slots;
 };
+
+// per group: wants of its first 4 children packed in bytes (0xFD: no child), for the
+// SIMD-compare child lookup of the tile kernels
+std::vector<uint32_t> group_wants(const Table &t) {
+    std::vector<uint32_t> out(t.groups.size());
+    for (size_t gi = 0; gi < t.groups.size(); gi++) {
+        uint32_t v = 0xFDFDFDFDu;
+        const DGroup &G = t.groups[gi];
+        for (uint32_t c = G.child_begin, k = 0; c < G.child_end && k < 4; c++, k++)
+            v = (v & ~(0xFFu << (8 * k))) | ((uint32_t)t.nodes[c].want << (8 * k));
+        out[gi] = v;
+    }
+    return out;
+}
+
+// Lane-kernel node rows: the DNode fields plus a completion-counter slot per node.
+std::vector<lane::LNode> lane_nodes(const Table &t, uint32_t &n_slots) {
+    std::vector<lane::LNode> out(t.nodes.size());
+    n_slots = 0;
+    for (size_t i = 0; i < t.nodes.size(); i++) {
+        const DNode &a = t.nodes[i];
+        lane::LNode &b = out[i];
+        b.want = a.want; b.n_new = a.n_new; b.nv = a.nv; b.flags = a.flags;
+        b.group_begin = a.group_begin; b.group_end = a.group_end;
+        b.slot = (a.flags & NODE_COMPLETION) ? (uint16_t)n_slots++ : (uint16_t)0xFFFF;
+        b.pad = 0;
+        if (a.flags & NODE_INNER) {  // pre-leaf: every child is a leaf
+            bool pre = true;
+            for (uint32_t gi = a.group_begin; gi < a.group_end; gi++)
+                for (uint32_t c = t.groups[gi].child_begin; c < t.groups[gi].child_end; c++)
+                    pre = pre && !(t.nodes[c].flags & NODE_INNER);
+            if (pre) b.flags |= bfs::NODE_PRELEAF;
+        }
+    }
+    return out;
+}
 
 bool small_table(uint32_t n_nodes, uint32_t n_groups) { return n_nodes <= kSmallRows && n_groups <= kSmallRows; }
 
@@ -840,26 +885,385 @@ cudaError_t launch_comine(const KParams &p, uint32_t max_vertices, bool stats, c
     return launch_comine_v<16>(p, stats, s, sms);
 }
 
+// ---- lane kernel (v3) launch: MAXV and counter mode by tree; grid = SMs x resident blocks
+template <int MAXV, bool LANECNT, bool STATS>
+cudaError_t launch_lane_t(const lane::LParams &p, size_t smem, cudaStream_t s, int sms) {
+    auto kern = lane::comine_lane_kernel<MAXV, LANECNT, STATS>;
+    static std::mutex mu;
+    static size_t cached_smem = 0;
+    static int cached_dev = -1, cached_per_sm = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (cached_smem == smem && cached_dev == dev) per_sm = cached_per_sm;
+    }
+    if (per_sm == 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, lane::kLB, smem);
+        if (e != cudaSuccess) return e;
+        if (per_sm < 1) per_sm = 1;
+        std::lock_guard<std::mutex> lk(mu);
+        cached_smem = smem;
+        cached_dev = dev;
+        cached_per_sm = per_sm;
+    }
+    uint32_t grid = (uint32_t)(sms * per_sm);
+    const uint32_t need = (p.n_roots + lane::kLB - 1) / lane::kLB;
+    if (need < grid) grid = need ? need : 1;
+    kern<<<grid, lane::kLB, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+constexpr size_t kLaneCntSmem = 48 * 1024;  // lane-private counters while they fit this budget
+
+template <int MAXV>
+cudaError_t launch_lane_v(const lane::LParams &p, bool stats, cudaStream_t s, int sms) {
+    const bool lanecnt = (size_t)p.n_slots * lane::kLB * 4 <= kLaneCntSmem;
+    const size_t smem = lane::smem_total(p.n_nodes, p.n_groups, p.n_slots, p.n_frames, lanecnt, MAXV);
+    if (lanecnt)
+        return stats ? launch_lane_t<MAXV, true, true>(p, smem, s, sms) : launch_lane_t<MAXV, true, false>(p, smem, s, sms);
+    return stats ? launch_lane_t<MAXV, false, true>(p, smem, s, sms) : launch_lane_t<MAXV, false, false>(p, smem, s, sms);
+}
+
+cudaError_t launch_lane(const lane::LParams &p, uint32_t max_vertices, bool stats, cudaStream_t s, int sms) {
+    if (max_vertices <= 4) return launch_lane_v<4>(p, stats, s, sms);
+    if (max_vertices <= 6) return launch_lane_v<6>(p, stats, s, sms);
+    if (max_vertices <= 8) return launch_lane_v<8>(p, stats, s, sms);
+    return launch_lane_v<16>(p, stats, s, sms);
+}
+
+// Kernel choice (MAYURA_KERNEL): "bfs" level-synchronous passes (v4, default), "lane" one
+// search per lane (v3), "warp" one search per warp (v2).  All three return identical counts.
+enum KernelKind { K_BFS = 0, K_LANE = 1, K_WARP = 2, K_WAVE = 3, K_TILE = 4, K_HYBRID = 5 };
+KernelKind kernel_kind() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MAYURA_KERNEL");
+        v = !e ? K_HYBRID : std::strcmp(e, "warp") == 0 ? K_WARP : std::strcmp(e, "lane") == 0 ? K_LANE
+          : std::strcmp(e, "bfs") == 0 ? K_BFS : std::strcmp(e, "wave") == 0 ? K_WAVE
+          : std::strcmp(e, "tile") == 0 ? K_TILE : K_HYBRID;
+    }
+    return (KernelKind)v;
+}
+// hybrid: BFS levels before the depth-first lane kernel (MAYURA_HYBRID_LEVELS, default 1)
+uint32_t hybrid_levels() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MAYURA_HYBRID_LEVELS");
+        v = e ? std::max(0, atoi(e)) : 1;
+    }
+    return (uint32_t)v;
+}
+bool use_warp_kernel() { return kernel_kind() == K_WARP; }
+
+// ---- BFS passes (v4): per level an expand pass and a long-window pass
+constexpr uint32_t kCtlWords = bfs::kStripes + 2;  // per level: stripe counters, long counter, pad
+
+template <int MAXV, bool L0, bool STATS>
+cudaError_t launch_bfs_pass(const bfs::BParams &p, bool long_pass, cudaStream_t s, int sms) {
+    auto kern = long_pass ? bfs::long_kernel<MAXV, L0, STATS> : bfs::expand_kernel<MAXV, L0, STATS>;
+    const size_t smem = bfs::smem_bytes(p.n_nodes, p.n_groups, p.n_slots, bfs::kTB);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bfs::kTB, smem);
+    if (e != cudaSuccess) return e;
+    uint32_t grid = (uint32_t)(sms * (per_sm > 0 ? per_sm : 1));
+    if (L0 && !long_pass) {
+        const uint32_t need = (p.n_roots + bfs::kTB - 1) / bfs::kTB;
+        grid = std::max(1u, std::min(grid, need));
+    }
+    kern<<<grid, bfs::kTB, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+template <int MAXV>
+cudaError_t launch_bfs_v(bfs::BParams &p, uint32_t levels, uint32_t *bufs[2], uint32_t *ctl, uint32_t seg_cap,
+                         bool stats, cudaStream_t s, int sms) {
+    for (uint32_t L = 0; L < levels; L++) {
+        p.in.data = L ? bufs[(L - 1) & 1] : nullptr;
+        p.in.cnt = L ? ctl + (L - 1) * kCtlWords : nullptr;
+        p.in.seg_cap = seg_cap;
+        p.out.data = bufs[L & 1];
+        p.out.cnt = ctl + L * kCtlWords;
+        p.out.seg_cap = seg_cap;
+        p.long_cnt = ctl + L * kCtlWords + bfs::kStripes;
+        for (int lp = 0; lp < 2; lp++) {
+            cudaError_t e;
+            if (L == 0) e = stats ? launch_bfs_pass<MAXV, true, true>(p, lp, s, sms) : launch_bfs_pass<MAXV, true, false>(p, lp, s, sms);
+            else e = stats ? launch_bfs_pass<MAXV, false, true>(p, lp, s, sms) : launch_bfs_pass<MAXV, false, false>(p, lp, s, sms);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_bfs(bfs::BParams &p, uint32_t max_vertices, uint32_t levels, uint32_t *bufs[2], uint32_t *ctl,
+                       uint32_t seg_cap, bool stats, cudaStream_t s, int sms) {
+    if (max_vertices <= 4) return launch_bfs_v<4>(p, levels, bufs, ctl, seg_cap, stats, s, sms);
+    if (max_vertices <= 6) return launch_bfs_v<6>(p, levels, bufs, ctl, seg_cap, stats, s, sms);
+    if (max_vertices <= 8) return launch_bfs_v<8>(p, levels, bufs, ctl, seg_cap, stats, s, sms);
+    return launch_bfs_v<16>(p, levels, bufs, ctl, seg_cap, stats, s, sms);
+}
+
+// ---- waves of window tasks (v5)
+constexpr uint32_t kWaveCtl = 3 * wave::kStripes;  // per wave: record, normal-task, long-task counters
+
+template <typename K>
+cudaError_t launch_wave_kernel(K kern, const wave::WParams &w, uint32_t items, cudaStream_t s, int sms) {
+    const size_t smem = wave::smem_bytes(w.n_nodes, w.n_groups, w.n_slots);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wave::kTB, smem);
+    if (e != cudaSuccess) return e;
+    uint32_t grid = (uint32_t)(sms * (per_sm > 0 ? per_sm : 1));
+    if (items) grid = std::max(1u, std::min(grid, (items + wave::kTB - 1) / wave::kTB));
+    kern<<<grid, wave::kTB, smem, s>>>(w);
+    return cudaGetLastError();
+}
+
+struct WaveBufs {
+    uint32_t *pm[2], *norm[2], *lng[2], *ctl;
+    uint32_t pm_seg_cap, norm_seg_cap, long_seg_cap;
+};
+
+template <int MAXV>
+cudaError_t launch_wave_v(wave::WParams &w, uint32_t waves, const WaveBufs &b, bool stats, cudaStream_t s, int sms) {
+    auto lists = [&](uint32_t k, wave::List &nl, wave::List &ll) {  // task lists written by wave k
+        nl.data = b.norm[k & 1]; nl.cnt = b.ctl + k * kWaveCtl + wave::kStripes; nl.seg_cap = b.norm_seg_cap;
+        ll.data = b.lng[k & 1]; ll.cnt = b.ctl + k * kWaveCtl + 2 * wave::kStripes; ll.seg_cap = b.long_seg_cap;
+    };
+    // wave 0: root windows
+    w.in_pm = nullptr;
+    w.in_tasks = wave::List{nullptr, nullptr, 0};
+    w.out_pm = b.pm[0]; w.out_pm_cnt = b.ctl; w.pm_seg_cap = b.pm_seg_cap;
+    lists(0, w.out_norm, w.out_long);
+    cudaError_t e = stats ? launch_wave_kernel(wave::root_kernel<MAXV, true>, w, w.n_roots, s, sms)
+                          : launch_wave_kernel(wave::root_kernel<MAXV, false>, w, w.n_roots, s, sms);
+    if (e != cudaSuccess) return e;
+    for (uint32_t k = 1; k <= waves; k++) {
+        wave::List in_n, in_l;
+        lists(k - 1, in_n, in_l);
+        w.in_pm = k >= 2 ? b.pm[(k - 2) & 1] : nullptr;     // records written by wave k-1
+        w.out_pm = b.pm[(k - 1) & 1];
+        w.out_pm_cnt = b.ctl + k * kWaveCtl;
+        lists(k, w.out_norm, w.out_long);
+        for (int lp = 0; lp < 2; lp++) {
+            w.in_tasks = lp ? in_l : in_n;
+            if (k == 1) {
+                if (lp) e = stats ? launch_wave_kernel(wave::scan_kernel<MAXV, 32, true, true>, w, 0, s, sms)
+                                  : launch_wave_kernel(wave::scan_kernel<MAXV, 32, true, false>, w, 0, s, sms);
+                else e = stats ? launch_wave_kernel(wave::scan_kernel<MAXV, wave::kSub, true, true>, w, 0, s, sms)
+                               : launch_wave_kernel(wave::scan_kernel<MAXV, wave::kSub, true, false>, w, 0, s, sms);
+            } else {
+                if (lp) e = stats ? launch_wave_kernel(wave::scan_kernel<MAXV, 32, false, true>, w, 0, s, sms)
+                                  : launch_wave_kernel(wave::scan_kernel<MAXV, 32, false, false>, w, 0, s, sms);
+                else e = stats ? launch_wave_kernel(wave::scan_kernel<MAXV, wave::kSub, false, true>, w, 0, s, sms)
+                               : launch_wave_kernel(wave::scan_kernel<MAXV, wave::kSub, false, false>, w, 0, s, sms);
+            }
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_wave(wave::WParams &w, uint32_t max_vertices, uint32_t waves, const WaveBufs &b, bool stats,
+                        cudaStream_t s, int sms) {
+    if (max_vertices <= 4) return launch_wave_v<4>(w, waves, b, stats, s, sms);
+    if (max_vertices <= 6) return launch_wave_v<6>(w, waves, b, stats, s, sms);
+    if (max_vertices <= 8) return launch_wave_v<8>(w, waves, b, stats, s, sms);
+    return launch_wave_v<16>(w, waves, b, stats, s, sms);
+}
+
+// Record / task / control buffers of the waves, allocated once per graph, grown on demand.
+// Capacities: records 8 per edge, normal tasks 12 per edge, long tasks 2 per edge
+// (each >= 2^20 and <= 2^26 items per buffer); overflow is handled in place (exact).
+mayura_status ensure_wave_buffers(mayura_graph_s *g, uint32_t words) {
+    auto segs = [&](uint64_t per_edge) {
+        return (uint32_t)((std::min<uint64_t>(std::max<uint64_t>(per_edge * g->E, 1u << 20), 1u << 26) +
+                           wave::kStripes - 1) / wave::kStripes);
+    };
+    uint32_t pm_seg = segs(8), n_seg = segs(12), l_seg = segs(2);
+    if (const char *e = getenv("MAYURA_BFS_SEG_CAP")) pm_seg = n_seg = l_seg = (uint32_t)std::max(1L, atol(e));
+    const size_t pm_bytes = (size_t)pm_seg * wave::kStripes * words * 4;
+    const size_t n_bytes = (size_t)n_seg * wave::kStripes * wave::kTaskWords * 4;
+    const size_t l_bytes = (size_t)l_seg * wave::kStripes * wave::kTaskWords * 4;
+    const size_t total = 2 * (pm_bytes + n_bytes + l_bytes) + sizeof(uint32_t) * (kWaveCtl * (bfs::kMaxLevels + 1) + 16);
+    if (g->wave_bytes < total) {
+        if (g->d_wave) cudaFree(g->d_wave);
+        g->d_wave = nullptr;
+        g->device_bytes -= g->wave_bytes;
+        g->wave_bytes = 0;
+        CK(cudaMalloc(&g->d_wave, total), "cudaMalloc(wave buffers)");
+        g->wave_bytes = total;
+        g->device_bytes += total;
+    }
+    g->wave_pm_seg = pm_seg; g->wave_n_seg = n_seg; g->wave_l_seg = l_seg;
+    g->wave_pm_bytes = pm_bytes; g->wave_n_bytes = n_bytes; g->wave_l_bytes = l_bytes;
+    return MAYURA_OK;
+}
+
+// ---- waves of window tiles (v6)
+template <typename K>
+cudaError_t launch_tile_kernel(K kern, const tile::TParams &w, uint32_t items, cudaStream_t s, int sms) {
+    const size_t smem = tile::smem_bytes(w.n_nodes, w.n_groups, w.n_slots);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tile::kTB, smem);
+    if (e != cudaSuccess) return e;
+    uint32_t grid = (uint32_t)(sms * (per_sm > 0 ? per_sm : 1));
+    if (items) grid = std::max(1u, std::min(grid, (items + tile::kTB - 1) / tile::kTB));
+    kern<<<grid, tile::kTB, smem, s>>>(w);
+    return cudaGetLastError();
+}
+
+struct TileBufs {
+    uint32_t *norm[2], *lng, *ctl;   // ctl: per wave k, [normal-task counters | long-task counters]
+    uint32_t norm_seg_cap, long_seg_cap;
+};
+
+template <int MAXV>
+cudaError_t launch_tile_v(tile::TParams &w, uint32_t waves, const TileBufs &b, bool stats, cudaStream_t s, int sms) {
+    auto nlist = [&](uint32_t k) {  // tasks of wave k
+        return wave::List{b.norm[k & 1], b.ctl + k * 2 * wave::kStripes, b.norm_seg_cap};
+    };
+    auto llist = [&](uint32_t k) {
+        return wave::List{b.lng, b.ctl + k * 2 * wave::kStripes + wave::kStripes, b.long_seg_cap};
+    };
+    cudaError_t e;
+    for (uint32_t k = 0; k < waves; k++) {
+        w.out_norm = nlist(k + 1);
+        w.out_long = llist(k);
+        if (k == 0) {
+            w.in_tasks = wave::List{nullptr, nullptr, 0};
+            e = stats ? launch_tile_kernel(tile::root_kernel<MAXV, true>, w, w.n_roots, s, sms)
+                      : launch_tile_kernel(tile::root_kernel<MAXV, false>, w, w.n_roots, s, sms);
+        } else {
+            w.in_tasks = nlist(k);
+            e = stats ? launch_tile_kernel(tile::tile_kernel<MAXV, true>, w, 0, s, sms)
+                      : launch_tile_kernel(tile::tile_kernel<MAXV, false>, w, 0, s, sms);
+        }
+        if (e != cudaSuccess) return e;
+        w.in_tasks = llist(k);
+        e = stats ? launch_tile_kernel(tile::long_kernel<MAXV, true>, w, 0, s, sms)
+                  : launch_tile_kernel(tile::long_kernel<MAXV, false>, w, 0, s, sms);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_tile(tile::TParams &w, uint32_t max_vertices, uint32_t waves, const TileBufs &b, bool stats,
+                        cudaStream_t s, int sms) {
+    if (max_vertices <= 4) return launch_tile_v<4>(w, waves, b, stats, s, sms);
+    if (max_vertices <= 6) return launch_tile_v<6>(w, waves, b, stats, s, sms);
+    if (max_vertices <= 8) return launch_tile_v<8>(w, waves, b, stats, s, sms);
+    return launch_tile_v<16>(w, waves, b, stats, s, sms);
+}
+
+uint32_t task_words(uint32_t max_vertices) {
+    const uint32_t mv = max_vertices <= 4 ? 4 : max_vertices <= 6 ? 6 : max_vertices <= 8 ? 8 : 16;
+    return (5 + mv + 3) & ~3u;
+}
+
+// Task lists of the tile waves, allocated once per graph and grown on demand: normal tasks
+// 8 per edge (x2, ping-pong), long tasks 2 per edge (each >= 2^20, <= 2^26 tasks);
+// overflow is mined in place (exact).
+mayura_status ensure_tile_buffers(mayura_graph_s *g, uint32_t words) {
+    auto segs = [&](uint64_t per_edge) {
+        return (uint32_t)((std::min<uint64_t>(std::max<uint64_t>(per_edge * g->E, 1u << 20), 1u << 26) +
+                           wave::kStripes - 1) / wave::kStripes);
+    };
+    uint32_t n_seg = segs(8), l_seg = segs(2);
+    if (const char *e = getenv("MAYURA_BFS_SEG_CAP")) n_seg = l_seg = (uint32_t)std::max(1L, atol(e));
+    const size_t n_bytes = (size_t)n_seg * wave::kStripes * words * 4;
+    const size_t l_bytes = (size_t)l_seg * wave::kStripes * words * 4;
+    const size_t ctl = sizeof(uint32_t) * (2 * wave::kStripes * (bfs::kMaxLevels + 1) + 16);
+    const size_t total = 2 * n_bytes + l_bytes + ctl;
+    if (g->tile_bytes < total) {
+        if (g->d_tile) cudaFree(g->d_tile);
+        g->d_tile = nullptr;
+        g->device_bytes -= g->tile_bytes;
+        g->tile_bytes = 0;
+        CK(cudaMalloc(&g->d_tile, total), "cudaMalloc(tile buffers)");
+        g->tile_bytes = total;
+        g->device_bytes += total;
+    }
+    g->tile_n_seg = n_seg; g->tile_l_seg = l_seg; g->tile_n_bytes = n_bytes; g->tile_l_bytes = l_bytes;
+    return MAYURA_OK;
+}
+
+uint32_t rec_words(uint32_t max_vertices) {
+    const uint32_t mv = max_vertices <= 4 ? 4 : max_vertices <= 6 ? 6 : max_vertices <= 8 ? 8 : 16;
+    return (8 + mv + 3) & ~3u;
+}
+
+// Frontier / long-item / control buffers of the BFS passes, allocated once per graph and
+// grown on demand.  Capacity: 4 records per edge (>= 2^20, <= 2^26) per buffer.
+mayura_status ensure_bfs_buffers(mayura_graph_s *g, uint32_t words) {
+    const uint64_t recs = std::min<uint64_t>(std::max<uint64_t>(8 * g->E, 1u << 20), 1u << 26);
+    uint32_t seg_cap = (uint32_t)((recs + bfs::kStripes - 1) / bfs::kStripes);
+    // test hook: tiny capacities force the depth-first fallback / in-place long windows
+    if (const char *e = getenv("MAYURA_BFS_SEG_CAP")) seg_cap = (uint32_t)std::max(1L, atol(e));
+    const size_t bytes = (size_t)seg_cap * bfs::kStripes * words * 4;
+    if (g->bfs_bytes < bytes) {
+        for (int i = 0; i < 2; i++)
+            if (g->d_bfs[i]) cudaFree(g->d_bfs[i]), g->d_bfs[i] = nullptr;
+        g->device_bytes -= 2 * g->bfs_bytes;
+        g->bfs_bytes = 0;
+        for (int i = 0; i < 2; i++) CK(cudaMalloc(&g->d_bfs[i], bytes), "cudaMalloc(frontier)");
+        g->bfs_bytes = bytes;
+        g->device_bytes += 2 * bytes;
+    }
+    g->bfs_seg_cap = std::min(seg_cap, (uint32_t)(g->bfs_bytes / ((size_t)bfs::kStripes * words * 4)));
+    if (!g->d_bfs_ctl) {
+        CK(cudaMalloc(&g->d_bfs_ctl, sizeof(uint32_t) * (kCtlWords * bfs::kMaxLevels + 16)), "cudaMalloc(bfs ctl)");
+        g->bfs_long_cap = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(g->E / 2, 1u << 20), 1u << 26);
+        if (const char *e = getenv("MAYURA_BFS_LONG_CAP")) g->bfs_long_cap = (uint32_t)std::max(1L, atol(e));
+        CK(cudaMalloc(&g->d_bfs_long, sizeof(uint32_t) * 3 * (size_t)g->bfs_long_cap), "cudaMalloc(long items)");
+        g->device_bytes += sizeof(uint32_t) * 3 * (size_t)g->bfs_long_cap;
+    }
+    return MAYURA_OK;
+}
+
 void table_view(const Table &t, uint32_t n_motifs, char *buf, DeviceTable &d) {
-    const size_t bn = t.nodes.size() * sizeof(DNode), bg = t.groups.size() * sizeof(DGroup);
+    const size_t bn = t.nodes.size() * sizeof(DNode), bg = t.groups.size() * sizeof(DGroup),
+                 bm = lane::align16(t.motif_node.size() * sizeof(uint32_t));
     d.nodes = reinterpret_cast<DNode *>(buf);
     d.groups = reinterpret_cast<DGroup *>(buf + bn);
     d.motif_node = reinterpret_cast<uint32_t *>(buf + bn + bg);
+    d.lnodes = reinterpret_cast<lane::LNode *>(buf + bn + bg + bm);
+    d.gwant = reinterpret_cast<uint32_t *>(buf + bn + bg + bm + lane::align16(t.nodes.size() * sizeof(lane::LNode)));
     d.n_nodes = (uint32_t)t.nodes.size();
     d.n_groups = (uint32_t)t.groups.size();
     d.n_motifs = n_motifs;
     d.max_vertices = t.max_vertices;
+    d.max_edges = t.max_edges;
+    d.n_slots = 0;
+    for (const DNode &x : t.nodes) d.n_slots += (x.flags & NODE_COMPLETION) ? 1 : 0;
 }
 
 mayura_status upload_table(const Table &t, uint32_t n_motifs, DeviceTable &d, void *&owner) {
     const size_t bn = t.nodes.size() * sizeof(DNode), bg = t.groups.size() * sizeof(DGroup),
-                 bm = t.motif_node.size() * sizeof(uint32_t);
+                 bm = t.motif_node.size() * sizeof(uint32_t), bm16 = lane::align16(bm);
+    uint32_t n_slots = 0;
+    const std::vector<lane::LNode> ln = lane_nodes(t, n_slots);
+    const size_t bl = lane::align16(ln.size() * sizeof(lane::LNode));
+    const std::vector<uint32_t> gw = group_wants(t);
     char *buf = nullptr;
-    CK(cudaMalloc(&buf, bn + bg + bm + 16), "cudaMalloc(mgtree table)");
+    CK(cudaMalloc(&buf, bn + bg + bm16 + bl + gw.size() * 4 + 16), "cudaMalloc(mgtree table)");
     owner = buf;
     CK(cudaMemcpy(buf, t.nodes.data(), bn, cudaMemcpyHostToDevice), "cudaMemcpy(table)");
     if (bg) CK(cudaMemcpy(buf + bn, t.groups.data(), bg, cudaMemcpyHostToDevice), "cudaMemcpy(table)");
     CK(cudaMemcpy(buf + bn + bg, t.motif_node.data(), bm, cudaMemcpyHostToDevice), "cudaMemcpy(table)");
+    CK(cudaMemcpy(buf + bn + bg + bm16, ln.data(), ln.size() * sizeof(lane::LNode), cudaMemcpyHostToDevice),
+       "cudaMemcpy(table)");
+    if (!gw.empty())
+        CK(cudaMemcpy(buf + bn + bg + bm16 + bl, gw.data(), gw.size() * 4, cudaMemcpyHostToDevice), "cudaMemcpy(table)");
     table_view(t, n_motifs, buf, d);
     return MAYURA_OK;
 }
@@ -953,6 +1357,16 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
         g->device_bytes += sizeof(uint32_t) * kCtxWords * (size_t)kCtxCap;
     }
     if (stats_host && !g->d_stats) CK(cudaMalloc(&g->d_stats, sizeof(unsigned long long) * ST_N), "cudaMalloc(stats)");
+    // MAYURA_DEBUG_WARPS=<file>: the instrumented lane kernel writes one timeline record per warp
+    // (start ns, end ns, iterations, warp-help batches, roots taken, root-queue-empty ns, SM id)
+    const char *dbg_path = stats_host ? getenv("MAYURA_DEBUG_WARPS") : nullptr;
+    const size_t kDbgWarps = 1u << 16;
+    if (dbg_path && !g->d_dbg) CK(cudaMalloc(&g->d_dbg, sizeof(unsigned long long) * 8 * kDbgWarps), "cudaMalloc(dbg)");
+    if (dbg_path) CK(cudaMemsetAsync(g->d_dbg, 0, sizeof(unsigned long long) * 8 * kDbgWarps, s), "cudaMemsetAsync(dbg)");
+    if (!dbg_path && stats_host && g->d_dbg) {
+        cudaFree(g->d_dbg);
+        g->d_dbg = nullptr;
+    }
     if (stats_host) CK(cudaMemsetAsync(g->d_stats, 0, sizeof(unsigned long long) * ST_N, s), "cudaMemsetAsync(stats)");
     const uint32_t n_roots = (uint32_t)(re - rb);
     const size_t n_launch = mode == 1 ? k : 1;
@@ -998,7 +1412,147 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
             if (p.epoch == 0) p.epoch = ++g->epoch;  // 0 marks a never-written slot
             p.counts = d_counts + (mode == 1 ? i : 0);
             p.stats = g->d_stats;
-            CK(launch_comine(p, dt.max_vertices, stats_host != nullptr, s, sms), "comine_kernel launch");
+            if (kernel_kind() == K_TILE) {
+                const uint32_t words = task_words(dt.max_vertices);
+                mayura_status ts = ensure_tile_buffers(g, words);
+                if (ts != MAYURA_OK) return ts;
+                char *base = reinterpret_cast<char *>(g->d_tile);
+                TileBufs tb;
+                tb.norm[0] = reinterpret_cast<uint32_t *>(base);
+                tb.norm[1] = reinterpret_cast<uint32_t *>(base + g->tile_n_bytes);
+                tb.lng = reinterpret_cast<uint32_t *>(base + 2 * g->tile_n_bytes);
+                tb.ctl = reinterpret_cast<uint32_t *>(base + 2 * g->tile_n_bytes + g->tile_l_bytes);
+                tb.norm_seg_cap = g->tile_n_seg; tb.long_seg_cap = g->tile_l_seg;
+                const size_t ctl_bytes = sizeof(uint32_t) * (2 * wave::kStripes * (bfs::kMaxLevels + 1) + 16);
+                CK(cudaMemsetAsync(tb.ctl, 0, ctl_bytes, s), "cudaMemsetAsync(tile ctl)");
+                tile::TParams w;
+                w.src = p.src; w.dst = p.dst; w.tr = p.tr; w.hi = p.hi; w.eptr = p.eptr;
+                w.out_off = p.out_off; w.in_off = p.in_off; w.out_ent = p.out_ent; w.in_ent = p.in_ent;
+                w.out_ptr = p.out_ptr; w.in_ptr = p.in_ptr;
+                w.nodes = dt.lnodes; w.groups = dt.groups; w.gwant = dt.gwant; w.motif_node = dt.motif_node;
+                w.n_nodes = dt.n_nodes; w.n_groups = dt.n_groups; w.n_motifs = dt.n_motifs; w.n_slots = dt.n_slots;
+                w.r0 = p.r0; w.n_roots = p.n_roots;
+                w.fallback = tb.ctl + 2 * wave::kStripes * (bfs::kMaxLevels + 1);
+                w.counts = p.counts; w.stats = p.stats;
+                const uint32_t waves = dt.max_edges > 1 ? dt.max_edges - 1 : 0;
+                if (waves == 0) {  // one-edge motifs only: the root kernel still counts roots
+                    w.in_tasks = wave::List{nullptr, nullptr, 0};
+                    w.out_norm = wave::List{tb.norm[1], tb.ctl, tb.norm_seg_cap};
+                    w.out_long = wave::List{tb.lng, tb.ctl + wave::kStripes, tb.long_seg_cap};
+                    if (dt.max_vertices <= 4)
+                        CK(stats_host ? launch_tile_kernel(tile::root_kernel<4, true>, w, w.n_roots, s, sms)
+                                      : launch_tile_kernel(tile::root_kernel<4, false>, w, w.n_roots, s, sms),
+                           "tile root launch");
+                } else {
+                    CK(launch_tile(w, dt.max_vertices, waves, tb, stats_host != nullptr, s, sms), "tile launch");
+                }
+            } else if (kernel_kind() == K_WAVE) {
+                const uint32_t words = rec_words(dt.max_vertices);
+                mayura_status ws = ensure_wave_buffers(g, words);
+                if (ws != MAYURA_OK) return ws;
+                char *base = reinterpret_cast<char *>(g->d_wave);
+                WaveBufs wb;
+                wb.pm[0] = reinterpret_cast<uint32_t *>(base);
+                wb.pm[1] = reinterpret_cast<uint32_t *>(base + g->wave_pm_bytes);
+                base += 2 * g->wave_pm_bytes;
+                wb.norm[0] = reinterpret_cast<uint32_t *>(base);
+                wb.norm[1] = reinterpret_cast<uint32_t *>(base + g->wave_n_bytes);
+                base += 2 * g->wave_n_bytes;
+                wb.lng[0] = reinterpret_cast<uint32_t *>(base);
+                wb.lng[1] = reinterpret_cast<uint32_t *>(base + g->wave_l_bytes);
+                base += 2 * g->wave_l_bytes;
+                wb.ctl = reinterpret_cast<uint32_t *>(base);
+                wb.pm_seg_cap = g->wave_pm_seg; wb.norm_seg_cap = g->wave_n_seg; wb.long_seg_cap = g->wave_l_seg;
+                const size_t ctl_bytes = sizeof(uint32_t) * (kWaveCtl * (bfs::kMaxLevels + 1) + 16);
+                CK(cudaMemsetAsync(wb.ctl, 0, ctl_bytes, s), "cudaMemsetAsync(wave ctl)");
+                wave::WParams w;
+                w.src = p.src; w.dst = p.dst; w.tr = p.tr; w.hi = p.hi; w.eptr = p.eptr;
+                w.out_off = p.out_off; w.in_off = p.in_off; w.out_ent = p.out_ent; w.in_ent = p.in_ent;
+                w.out_ptr = p.out_ptr; w.in_ptr = p.in_ptr;
+                w.nodes = dt.lnodes; w.groups = dt.groups; w.motif_node = dt.motif_node;
+                w.n_nodes = dt.n_nodes; w.n_groups = dt.n_groups; w.n_motifs = dt.n_motifs; w.n_slots = dt.n_slots;
+                w.r0 = p.r0; w.n_roots = p.n_roots;
+                w.fallback = wb.ctl + kWaveCtl * (bfs::kMaxLevels + 1);
+                w.counts = p.counts; w.stats = p.stats;
+                const uint32_t waves = dt.max_edges > 1 ? dt.max_edges - 1 : 0;
+                CK(launch_wave(w, dt.max_vertices, waves, wb, stats_host != nullptr, s, sms), "wave launch");
+            } else if (kernel_kind() == K_HYBRID) {
+                // BFS over the first levels (splits heavy roots into many partial matches),
+                // then one depth-first search per partial match in the lane kernel
+                const uint32_t words = rec_words(dt.max_vertices);
+                uint32_t levels = std::min(hybrid_levels(), dt.max_edges > 2 ? dt.max_edges - 2 : 0u);
+                lane::LParams q;
+                q.src = p.src; q.dst = p.dst; q.tr = p.tr; q.hi = p.hi; q.eptr = p.eptr;
+                q.out_off = p.out_off; q.in_off = p.in_off; q.out_ent = p.out_ent; q.in_ent = p.in_ent;
+                q.out_ptr = p.out_ptr; q.in_ptr = p.in_ptr;
+                q.nodes = dt.lnodes; q.groups = dt.groups; q.motif_node = dt.motif_node;
+                q.n_nodes = dt.n_nodes; q.n_groups = dt.n_groups; q.n_motifs = dt.n_motifs; q.n_slots = dt.n_slots;
+                q.n_frames = dt.max_edges > 2 ? dt.max_edges - 2 : 0;
+                q.r0 = p.r0; q.n_roots = p.n_roots; q.lb = p.lb; q.counts = p.counts; q.stats = p.stats;
+                q.dbg = stats_host ? g->d_dbg : nullptr;
+                q.pm = nullptr; q.pm_cnt = nullptr; q.pm_seg_cap = 0; q.pm_words = words;
+                if (levels > 0) {
+                    mayura_status bs = ensure_bfs_buffers(g, words);
+                    if (bs != MAYURA_OK) return bs;
+                    uint32_t *ctl = g->d_bfs_ctl;
+                    CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * (kCtlWords * bfs::kMaxLevels + 16), s),
+                       "cudaMemsetAsync(ctl)");
+                    bfs::BParams b;
+                    b.src = p.src; b.dst = p.dst; b.tr = p.tr; b.hi = p.hi; b.eptr = p.eptr;
+                    b.out_off = p.out_off; b.in_off = p.in_off; b.out_ent = p.out_ent; b.in_ent = p.in_ent;
+                    b.out_ptr = p.out_ptr; b.in_ptr = p.in_ptr;
+                    b.nodes = dt.lnodes; b.groups = dt.groups; b.motif_node = dt.motif_node;
+                    b.n_nodes = dt.n_nodes; b.n_groups = dt.n_groups; b.n_motifs = dt.n_motifs;
+                    b.n_slots = dt.n_slots;
+                    b.r0 = p.r0; b.n_roots = p.n_roots;
+                    b.long_items = g->d_bfs_long; b.long_cap = g->bfs_long_cap;
+                    b.fallback = ctl + kCtlWords * bfs::kMaxLevels;
+                    b.inline_preleaf = 0;
+                    b.counts = p.counts; b.stats = p.stats;
+                    uint32_t *bufs[2] = {g->d_bfs[0], g->d_bfs[1]};
+                    CK(launch_bfs(b, dt.max_vertices, levels, bufs, ctl, g->bfs_seg_cap, stats_host != nullptr, s,
+                                  sms), "bfs pass launch");
+                    q.pm = bufs[(levels - 1) & 1];
+                    q.pm_cnt = ctl + (levels - 1) * kCtlWords;
+                    q.pm_seg_cap = g->bfs_seg_cap;
+                }
+                CK(launch_lane(q, dt.max_vertices, stats_host != nullptr, s, sms), "comine_lane_kernel launch");
+            } else if (kernel_kind() == K_BFS) {
+                const uint32_t words = rec_words(dt.max_vertices);
+                mayura_status bs = ensure_bfs_buffers(g, words);
+                if (bs != MAYURA_OK) return bs;
+                uint32_t *ctl = g->d_bfs_ctl;
+                CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * (kCtlWords * bfs::kMaxLevels + 16), s), "cudaMemsetAsync(ctl)");
+                bfs::BParams b;
+                b.src = p.src; b.dst = p.dst; b.tr = p.tr; b.hi = p.hi; b.eptr = p.eptr;
+                b.out_off = p.out_off; b.in_off = p.in_off; b.out_ent = p.out_ent; b.in_ent = p.in_ent;
+                b.out_ptr = p.out_ptr; b.in_ptr = p.in_ptr;
+                b.nodes = dt.lnodes; b.groups = dt.groups; b.motif_node = dt.motif_node;
+                b.n_nodes = dt.n_nodes; b.n_groups = dt.n_groups; b.n_motifs = dt.n_motifs; b.n_slots = dt.n_slots;
+                b.r0 = p.r0; b.n_roots = p.n_roots;
+                b.long_items = g->d_bfs_long; b.long_cap = g->bfs_long_cap;
+                b.fallback = ctl + kCtlWords * bfs::kMaxLevels;
+                b.inline_preleaf = 1;
+                b.counts = p.counts; b.stats = p.stats;
+                uint32_t *bufs[2] = {g->d_bfs[0], g->d_bfs[1]};
+                const uint32_t levels = dt.max_edges > 1 ? dt.max_edges - 1 : 1;
+                CK(launch_bfs(b, dt.max_vertices, levels, bufs, ctl, g->bfs_seg_cap, stats_host != nullptr, s, sms),
+                   "bfs pass launch");
+            } else if (use_warp_kernel()) {
+                CK(launch_comine(p, dt.max_vertices, stats_host != nullptr, s, sms), "comine_kernel launch");
+            } else {
+                lane::LParams q;
+                q.src = p.src; q.dst = p.dst; q.tr = p.tr; q.hi = p.hi; q.eptr = p.eptr;
+                q.out_off = p.out_off; q.in_off = p.in_off; q.out_ent = p.out_ent; q.in_ent = p.in_ent;
+                q.out_ptr = p.out_ptr; q.in_ptr = p.in_ptr;
+                q.nodes = dt.lnodes; q.groups = dt.groups; q.motif_node = dt.motif_node;
+                q.n_nodes = dt.n_nodes; q.n_groups = dt.n_groups; q.n_motifs = dt.n_motifs; q.n_slots = dt.n_slots;
+                q.n_frames = dt.max_edges > 2 ? dt.max_edges - 2 : 0;
+                q.r0 = p.r0; q.n_roots = p.n_roots; q.lb = p.lb; q.counts = p.counts; q.stats = p.stats;
+                q.dbg = stats_host ? g->d_dbg : nullptr;
+                q.pm = nullptr; q.pm_cnt = nullptr; q.pm_seg_cap = 0; q.pm_words = 0;
+                CK(launch_lane(q, dt.max_vertices, stats_host != nullptr, s, sms), "comine_lane_kernel launch");
+            }
         }
     }
     if (stats_host) {
@@ -1009,7 +1563,23 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
         CK(cudaMemcpyAsync(counts_out, d_counts, sizeof(unsigned long long) * k, cudaMemcpyDeviceToHost, s),
            "cudaMemcpyAsync(counts)");
     }
-    if (!on_device || stats_host) CK(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    if (!on_device || stats_host) {
+        CK(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        if (dbg_path && g->d_dbg) {
+            std::vector<unsigned long long> rec(8 * kDbgWarps);
+            CK(cudaMemcpy(rec.data(), g->d_dbg, rec.size() * 8, cudaMemcpyDeviceToHost), "cudaMemcpy(dbg)");
+            if (FILE *f = fopen(dbg_path, "wb")) {
+                fwrite(rec.data(), 8, rec.size(), f);
+                fclose(f);
+            }
+        }
+        // the lane kernel's load-balancer watchdog (never expected to fire) marks LB_ERR
+        std::vector<uint32_t> lbw(n_lb);
+        CK(cudaMemcpy(lbw.data(), g->d_queue, sizeof(uint32_t) * n_lb, cudaMemcpyDeviceToHost), "cudaMemcpy(lb)");
+        for (size_t i = 0; i < n_launch; i++)
+            if (lbw[LB_N * i + LB_ERR])
+                return fail(MAYURA_E_CUDA, "mayura_comine: load-balancer watchdog fired (counts invalid)");
+    }
     return MAYURA_OK;
 }
 
@@ -1018,7 +1588,8 @@ void free_device(mayura_graph_s *g) {
     DeviceGuard guard(g->device);
     void *ptrs[] = {g->d_src, g->d_dst, g->d_tr, g->d_hi, g->d_t, g->d_out_off, g->d_in_off, g->d_out_ent,
                     g->d_in_ent, g->d_eptr, g->d_out_ptr, g->d_in_ptr, g->d_ctx, g->d_queue, g->d_counts,
-                    g->d_stats};
+                    g->d_stats, g->d_dbg, g->d_bfs[0], g->d_bfs[1], g->d_bfs_ctl, g->d_bfs_long,
+                    g->d_wave, g->d_tile};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }

@@ -88,6 +88,17 @@ struct mayura_graph_s {
     unsigned long long *d_counts = nullptr;              // scratch counts (host-output calls)
     uint32_t d_counts_cap = 0;
     unsigned long long *d_stats = nullptr;
+    unsigned long long *d_dbg = nullptr;                 // MAYURA_DEBUG_WARPS timeline
+    uint32_t *d_bfs[2] = {nullptr, nullptr};             // BFS frontier buffers (ping-pong)
+    uint32_t *d_bfs_ctl = nullptr, *d_bfs_long = nullptr;
+    size_t bfs_bytes = 0;
+    uint32_t bfs_seg_cap = 0, bfs_long_cap = 0;
+    uint32_t *d_wave = nullptr;                          // wave records + task lists + counters
+    size_t wave_bytes = 0, wave_pm_bytes = 0, wave_n_bytes = 0, wave_l_bytes = 0;
+    uint32_t wave_pm_seg = 0, wave_n_seg = 0, wave_l_seg = 0;
+    uint32_t *d_tile = nullptr;                          // tile task lists + counters
+    size_t tile_bytes = 0, tile_n_bytes = 0, tile_l_bytes = 0;
+    uint32_t tile_n_seg = 0, tile_l_seg = 0;
     uint64_t device_bytes = 0;
 };
 

@@ -1,0 +1,588 @@
+// lane.cuh -- lane-per-search co-mining kernel (kernel v3), included by comine.cu.
+//
+// Algorithm 3 "Co-Mining" with one search per ROOT EDGE per LANE:
+// every lane of a warp walks the MG-Tree table depth-first for its own root (the
+// paper's thread-per-first-edge mapping), so a warp makes progress
+// on 32 independent searches at once.  Profiles of the warp-per-root kernel (v2,
+// profiles/r01_*.md) showed windows average ~2 entries: a whole warp per window spent
+// ~2,200 issue slots per root on warp-uniform overhead.  Here every loop iteration
+// processes ONE window entry (or one control transition) per lane, with a body of a
+// few dozen instructions that all lanes execute in lockstep:
+//   - window start (Algo 1 l.210-214): successor pointers P(e) of the edge matched at
+//     the node (exact), the root's R (lower bound; pre-window entries are skipped by
+//     the time test), a per-lane binary search (other anchors), or a binary search of
+//     the edge array (GLOBAL anchor, reading R6);
+//   - candidate test (Algo 1 l.219 + full injectivity R4): classify the neighbour
+//     against the lane's m2g registers -> which mapped motif vertex it is, or NEW;
+//     in an anchor group at most one child wants a given class;
+//   - completion child: count[Q_N]++ (Algo 3 l.661) in a lane-private shared-memory
+//     counter; inner child: push a frame (lane-private shared memory) and descend
+//     (Algo 3 l.665-669); window end ("time rank > hi(root)", sentinel-terminated
+//     lists) -> next anchor group -> pop.
+// Roots are handed out by a warp-aggregated atomic cursor (guided chunk sizes):
+// a lane that finishes its search takes the next root at the next iteration.
+// Long windows (>= kHelpMin entries) are not scanned lane-serially: the lane parks the
+// window and the whole warp scans it 32 entries per step (coalesced loads, ballot per
+// child), queueing descents back to the owning lane -- see `warp_help`.
+
+namespace lane {
+
+constexpr int kLB = 128;                 // threads per block
+constexpr int kFrameWords = 8;           // node|g<<16, pos, tr_prev, lim, P.x, P.y, P.z, P.w
+constexpr uint32_t kHelpMin = 12;       // leaf windows of >= this many entries are scanned by the warp
+constexpr uint32_t kAgeMin = 64;        // steps on one search before its descents are handed out
+constexpr uint32_t kStackCap = 32;      // per-warp task stack (tasks)
+constexpr int kPmStripes = 64;          // segments of a partial-match source (bfs::kStripes)
+
+struct __align__(4) LNode {  // 12 bytes
+    uint8_t want, n_new, nv, flags;
+    uint16_t group_begin, group_end;
+    uint16_t slot;                      // completion counter slot (0xFFFF: none)
+    uint16_t pad;
+};
+
+struct LParams {
+    const uint32_t *src, *dst, *tr, *hi;
+    const uint4 *eptr;
+    const uint32_t *out_off, *in_off;
+    const uint2 *out_ent, *in_ent;
+    const uint4 *out_ptr, *in_ptr;
+    const LNode *nodes;
+    const DGroup *groups;
+    const uint32_t *motif_node;
+    uint32_t n_nodes, n_groups, n_motifs, n_slots, n_frames;
+    uint32_t r0, n_roots;
+    uint32_t *lb;                       // load-balancer words (LB_*), zeroed per launch
+    unsigned long long *dbg;            // STATS + debug: per-warp timeline records (or null)
+    // hybrid mode: the searches start from partial matches a BFS pass wrote (striped
+    // records: node|nv<<16, root, tr_prev, h, P, m2g) instead of from root edges
+    const uint32_t *pm;                 // null: root edges [r0, r0 + n_roots)
+    const uint32_t *pm_cnt;             // kPmStripes counters
+    uint32_t pm_seg_cap, pm_words;
+    unsigned long long *counts;
+    unsigned long long *stats;
+};
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// dynamic shared memory layout: nodes | groups | slot totals (u64) | lane counters (u32,
+// LANECNT only) | frames
+__host__ __device__ inline size_t off_groups(uint32_t nn) { return align16((size_t)nn * sizeof(LNode)); }
+__host__ __device__ inline size_t off_tot(uint32_t nn, uint32_t ng) { return off_groups(nn) + align16((size_t)ng * sizeof(DGroup)); }
+__host__ __device__ inline size_t off_cnt(uint32_t nn, uint32_t ng, uint32_t ns) {
+    return off_tot(nn, ng) + align16((size_t)ns * 8);
+}
+__host__ __device__ inline size_t off_frames(uint32_t nn, uint32_t ng, uint32_t ns, bool lanecnt) {
+    return off_cnt(nn, ng, ns) + (lanecnt ? (size_t)ns * kLB * 4 : 0);
+}
+__host__ __device__ inline size_t smem_total(uint32_t nn, uint32_t ng, uint32_t ns, uint32_t nf, bool lanecnt,
+                                             int maxv) {
+    return off_frames(nn, ng, ns, lanecnt) + (size_t)(nf ? nf : 1) * kFrameWords * kLB * 4 +
+           (size_t)(kLB / 32) * (11 + maxv) * kStackCap * 4;
+}
+
+// m2g[k] == kNone for every motif vertex k that is not mapped (k >= nv), so the class
+// of a graph vertex is one compare per slot (vertex ids are < 2^31).
+template <int MAXV>
+__device__ __forceinline__ uint32_t classify(const uint32_t (&m)[MAXV], uint32_t x) {
+    uint32_t c = CLS_NEW;
+#pragma unroll
+    for (int k = 0; k < MAXV; k++) c = (m[k] == x) ? (uint32_t)k : c;
+    return c;
+}
+// Opaque select: keeps m2g in registers (the compiler otherwise re-rolls the unrolled
+// select chains into an indexed local-memory array).
+__device__ __forceinline__ uint32_t selp(uint32_t a, uint32_t b, bool c) {
+    uint32_t r;
+    asm("{ .reg .pred q; setp.ne.u32 q, %3, 0; selp.b32 %0, %1, %2, q; }" : "=r"(r) : "r"(a), "r"(b), "r"((uint32_t)c));
+    return r;
+}
+template <int MAXV>
+__device__ __forceinline__ void m2g_set(uint32_t (&m)[MAXV], uint32_t i, uint32_t x) {
+#pragma unroll
+    for (int k = 0; k < MAXV; k++) m[k] = selp(x, m[k], k == (int)i);
+}
+template <int MAXV>
+__device__ __forceinline__ uint32_t m2g_get(const uint32_t (&m)[MAXV], uint32_t i) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int k = 0; k < MAXV; k++) r = selp(m[k], r, k == (int)i);
+    return r;
+}
+__device__ __forceinline__ uint32_t pick4(const uint4 &v, uint32_t k) {
+    return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+}
+
+template <int MAXV, bool LANECNT, bool STATS>
+__global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_constant__ LParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    LNode *s_nodes = reinterpret_cast<LNode *>(smem);
+    DGroup *s_groups = reinterpret_cast<DGroup *>(smem + off_groups(p.n_nodes));
+    unsigned long long *s_tot = reinterpret_cast<unsigned long long *>(smem + off_tot(p.n_nodes, p.n_groups));
+    uint32_t *s_cnt = reinterpret_cast<uint32_t *>(smem + off_cnt(p.n_nodes, p.n_groups, p.n_slots));
+    uint32_t *s_fr = reinterpret_cast<uint32_t *>(smem + off_frames(p.n_nodes, p.n_groups, p.n_slots, LANECNT));
+    uint32_t *s_stk = s_fr + (size_t)(p.n_frames ? p.n_frames : 1) * kFrameWords * kLB;
+    __shared__ uint32_t s_pref[kPmStripes + 1];
+    if (p.pm && threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (int i = 0; i < kPmStripes; i++) {
+            s_pref[i] = acc;
+            acc += min(p.pm_cnt[i], p.pm_seg_cap);
+        }
+        s_pref[kPmStripes] = acc;
+    }
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (uint32_t i = tid; i < p.n_nodes; i += kLB) s_nodes[i] = p.nodes[i];
+    for (uint32_t i = tid; i < p.n_groups; i += kLB) s_groups[i] = p.groups[i];
+    for (uint32_t i = tid; i < p.n_slots; i += kLB) s_tot[i] = 0;
+    if (LANECNT)
+        for (uint32_t i = 0; i < p.n_slots; i++) s_cnt[i * kLB + tid] = 0;
+    __syncthreads();
+
+    uint32_t *myfr = s_fr + tid;    // frame d, word f at myfr[(d * kFrameWords + f) * kLB]
+    uint32_t *wstk = s_stk + (size_t)(tid >> 5) * (11 + MAXV) * kStackCap;  // word q of slot i: [q * kStackCap + i]
+    const uint32_t wbase = (uint32_t)tid & ~31u;
+    // add n matches to lane `ln`'s counter of `slot` (ln = this lane, or a parked lane of
+    // this warp whose window the warp scans for it)
+    auto count_n = [&](uint32_t slot, uint32_t ln, uint32_t n) {
+        if (LANECNT) {
+            uint32_t *c = s_cnt + slot * kLB + ln;
+            uint32_t v = *c + n;
+            if (v >= 0x80000000u) {
+                atomicAdd(&s_tot[slot], (unsigned long long)v);
+                v = 0;
+            }
+            *c = v;
+        } else {
+            atomicAdd(&s_tot[slot], (unsigned long long)n);
+        }
+    };
+    unsigned long long st[ST_N];
+#pragma unroll
+    for (int i = 0; i < ST_N; i++) st[i] = 0;
+
+    const LNode root = s_nodes[0];
+    const bool root_inner = (root.flags & NODE_INNER) != 0;
+    const uint32_t n_items = p.pm ? s_pref[kPmStripes] : p.n_roots;
+
+    // ------------------------------------------------------------ lane state
+    bool active = false, scan = false, help = false, fresh = false;
+    uint32_t age = 0;                  // steps since this lane took its root / task
+    uint32_t stop = 0;                 // warp-uniform: tasks on this warp's stack
+    uint32_t m2g[MAXV];
+#pragma unroll
+    for (int k = 0; k < MAXV; k++) m2g[k] = kNone;
+    uint32_t h = 0, tr_prev = 0, node = 0, nv = 2, g = 0, g_end = 0, pos = 0, lim = kNone, d = 0;
+    uint4 P = make_uint4(0, 0, 0, 0), R = make_uint4(0, 0, 0, 0);
+
+    // warp-uniform root chunk
+    uint32_t cb = 0, cl = 0;
+    bool roots_left = true;
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    unsigned long long t_start = 0, n_iter = 0, n_help = 0, n_roots_w = 0, t_roots_done = 0;
+    if (STATS && p.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    for (;;) {
+        if (STATS && p.dbg) {
+            n_iter++;
+            if (!roots_left && t_roots_done == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_roots_done));
+        }
+        // ---------------------------------------------------- (0) this warp's task stack first
+        // Partial matches handed out by heavy lanes (section 2) wait in a per-warp LIFO in
+        // shared memory; idle lanes pop them before taking new roots.  The warp runs this
+        // loop in lockstep, so the stack needs no atomics (ballot ranks + a uniform top).
+        {
+            const unsigned needq = __ballot_sync(kFull, !active);
+            const uint32_t k = min((uint32_t)__popc(needq), stop);
+            if (k) {
+                __syncwarp();
+                const uint32_t rank = __popc(needq & lt_mask);
+                if (((needq >> lane) & 1u) && rank < k) {
+                    const uint32_t slot = stop - 1 - rank;
+                    const uint32_t w0 = wstk[0 * kStackCap + slot];
+                    node = w0 & 0xffffu;
+                    nv = w0 >> 16;
+                    tr_prev = wstk[1 * kStackCap + slot];
+                    h = wstk[2 * kStackCap + slot];
+                    P = make_uint4(wstk[3 * kStackCap + slot], wstk[4 * kStackCap + slot], wstk[5 * kStackCap + slot],
+                                   wstk[6 * kStackCap + slot]);
+                    R = make_uint4(wstk[7 * kStackCap + slot], wstk[8 * kStackCap + slot], wstk[9 * kStackCap + slot],
+                                   wstk[10 * kStackCap + slot]);
+#pragma unroll
+                    for (int q = 0; q < MAXV; q++) m2g[q] = wstk[(11 + q) * kStackCap + slot];
+                    const LNode dn = s_nodes[node];
+                    g = dn.group_begin;
+                    g_end = dn.group_end;
+                    lim = kNone; d = 0; scan = false; active = true; age = 0;
+                    if (STATS) st[ST_CONTEXTS]++;
+                }
+                stop -= k;
+                __syncwarp();
+            }
+        }
+
+        // ---------------------------------------------------- (1) roots for the rest
+        unsigned need = __ballot_sync(kFull, !active);
+        while (need && roots_left) {
+            if (cl == 0) {
+                uint32_t b = 0, sz = 0;
+                if (lane == 0) {
+                    const uint32_t cur = *(volatile uint32_t *)(p.lb + LB_ROOT);
+                    const uint32_t rem = cur < n_items ? n_items - cur : 0u;
+                    sz = max(32u, min(256u, rem / (4u * gridDim.x * (kLB / 32))));
+                    b = atomicAdd(p.lb + LB_ROOT, sz);
+                }
+                b = __shfl_sync(kFull, b, 0);
+                sz = __shfl_sync(kFull, sz, 0);
+                if (b >= n_items) {
+                    roots_left = false;
+                    break;
+                }
+                cb = b;
+                cl = min(sz, n_items - b);
+            }
+            const uint32_t take = min((uint32_t)__popc(need), cl);
+            const uint32_t rank = __popc(need & lt_mask);
+            const bool mine = ((need >> lane) & 1u) && rank < take;
+            if (mine && p.pm) {  // a partial match: its node's completion was counted when it was made
+                const uint32_t item = cb + rank;
+                int lo = 0, hi2 = kPmStripes - 1;
+                while (lo < hi2) {
+                    const int mid = (lo + hi2 + 1) >> 1;
+                    if (s_pref[mid] <= item) lo = mid;
+                    else hi2 = mid - 1;
+                }
+                const uint4 *rec = reinterpret_cast<const uint4 *>(
+                    p.pm + ((size_t)lo * p.pm_seg_cap + (item - s_pref[lo])) * p.pm_words);
+                const uint4 a = __ldcs(rec), b4 = __ldcs(rec + 1);
+                node = a.x & 0xffffu;
+                nv = a.x >> 16;
+                const uint32_t rt = a.y;
+                tr_prev = a.z;
+                h = a.w;
+                P = b4;
+#pragma unroll
+                for (int q = 0; q < (MAXV + 3) / 4; q++) {
+                    const uint4 m4 = __ldcs(rec + 2 + q);
+                    if (4 * q + 0 < MAXV) m2g[(4 * q + 0) % MAXV] = m4.x;
+                    if (4 * q + 1 < MAXV) m2g[(4 * q + 1) % MAXV] = m4.y;
+                    if (4 * q + 2 < MAXV) m2g[(4 * q + 2) % MAXV] = m4.z;
+                    if (4 * q + 3 < MAXV) m2g[(4 * q + 3) % MAXV] = m4.w;
+                }
+                R = __ldg(p.eptr + rt);
+                const LNode dn = s_nodes[node];
+                g = dn.group_begin; g_end = dn.group_end;
+                lim = kNone; d = 0; scan = false; age = 0;
+                active = true;
+            } else if (mine) {
+                const uint32_t r = p.r0 + cb + rank;
+                const uint32_t rs = __ldg(p.src + r), rd = __ldg(p.dst + r);
+                if (rs != rd) {  // a self-loop never matches canonical 0->1 (reading R7)
+                    if (root.flags & NODE_COMPLETION) count_n(root.slot, tid, 1);
+                    if (STATS) {
+                        st[ST_ROOTS]++;
+                        st[ST_BYTES] += 16 + (root_inner ? 16 : 0);
+                        st[ST_MATCHES] += (root.flags & NODE_COMPLETION) ? 1 : 0;
+                    }
+                    if (root_inner) {
+#pragma unroll
+                        for (int k = 2; k < MAXV; k++) m2g[k] = kNone;
+                        m2g[0] = rs;
+                        m2g[1] = rd;
+                        h = __ldg(p.hi + r);
+                        tr_prev = __ldg(p.tr + r);
+                        R = __ldg(p.eptr + r);
+                        P = R;
+                        node = 0; nv = 2; g = root.group_begin; g_end = root.group_end;
+                        lim = kNone; d = 0; scan = false; age = 0;
+                        active = true;
+                        if (STATS) st[ST_NODES]++;
+                    }
+                } else if (STATS) {
+                    st[ST_BYTES] += 16;
+                }
+            }
+            const unsigned served = __ballot_sync(kFull, mine);
+            if (STATS) n_roots_w += __popc(served);
+            need &= ~served;
+            cb += take;
+            cl -= take;
+        }
+
+        // ---------------------------------------------------- one step of this lane's search
+        fresh = false;
+        do {
+            if (!active) break;
+            ++age;
+            if (!scan) {
+                if (g == g_end) {  // all anchor groups of `node` done: pop
+                    if (d == 0) {
+                        active = false;
+                        break;
+                    }
+                    --d;
+                    const uint32_t w0 = myfr[(d * kFrameWords + 0) * kLB];
+                    pos = myfr[(d * kFrameWords + 1) * kLB];
+                    tr_prev = myfr[(d * kFrameWords + 2) * kLB];
+                    lim = myfr[(d * kFrameWords + 3) * kLB];
+                    P.x = myfr[(d * kFrameWords + 4) * kLB];
+                    P.y = myfr[(d * kFrameWords + 5) * kLB];
+                    P.z = myfr[(d * kFrameWords + 6) * kLB];
+                    P.w = myfr[(d * kFrameWords + 7) * kLB];
+                    node = w0 & 0xffffu;
+                    g = w0 >> 16;
+                    const LNode dn = s_nodes[node];
+                    nv = dn.nv;
+                    g_end = dn.group_end;
+#pragma unroll
+                    for (int k = 2; k < MAXV; k++) m2g[k] = selp(m2g[k], kNone, (uint32_t)k < nv);
+                } else {
+                    const DGroup G = s_groups[g];
+                    if (G.start < START_R0) {
+                        pos = pick4(P, G.start);
+                        lim = kNone;
+                    } else if (G.start < START_SEARCH) {
+                        pos = pick4(R, G.start - START_R0);
+                        lim = kNone;
+                    } else if (G.start == START_SEARCH) {
+                        const uint32_t x = m2g_get<MAXV>(m2g, G.anchor);
+                        const uint32_t *off = (G.kind == ANCHOR_OUT) ? p.out_off : p.in_off;
+                        const uint2 *ent = (G.kind == ANCHOR_OUT) ? p.out_ent : p.in_ent;
+                        uint32_t lo = __ldg(off + x), hi2 = __ldg(off + x + 1) - 1;
+                        while (lo < hi2) {  // first entry with time rank > tr_prev
+                            const uint32_t mid = lo + ((hi2 - lo) >> 1);
+                            if (__ldg(&ent[mid].x) > tr_prev) hi2 = mid;
+                            else lo = mid + 1;
+                            if (STATS) st[ST_PROBES]++;
+                        }
+                        pos = lo;
+                        lim = kNone;
+                        if (STATS) st[ST_BYTES] += 8;
+                    } else {  // GLOBAL: edge ids after the tie group of the previous edge, up to hi(root)
+                        uint32_t lo = tr_prev, hi2 = h + 1;
+                        while (lo < hi2) {
+                            const uint32_t mid = lo + ((hi2 - lo) >> 1);
+                            if (__ldg(p.tr + mid) > tr_prev) hi2 = mid;
+                            else lo = mid + 1;
+                            if (STATS) st[ST_PROBES]++;
+                        }
+                        pos = lo;
+                        lim = h + 1;
+                    }
+                    if (STATS) {
+                        st[ST_WINDOWS]++;
+                        st[ST_BYTES] += G.kind == ANCHOR_GLOBAL ? 12 : 8;  // the terminating entry
+                    }
+                    // a long window of leaf children is scanned by the whole warp (below)
+                    if (G.n_inner == 0 && G.kind != ANCHOR_GLOBAL) {
+                        const uint2 *ent = (G.kind == ANCHOR_OUT) ? p.out_ent : p.in_ent;
+                        if (__ldg(&ent[pos + kHelpMin - 1].x) <= h) {
+                            help = true;
+                            break;
+                        }
+                    }
+                }
+                scan = true;
+            }
+
+            // scan one entry of the current window
+            const DGroup G = s_groups[g];
+            uint32_t etr, e1, e2 = 0;
+            const bool glob = G.kind == ANCHOR_GLOBAL;
+            if (glob) {
+                etr = pos < lim ? __ldg(p.tr + pos) : kNone;
+                if (etr != kNone) {
+                    e1 = __ldg(p.src + pos);
+                    e2 = __ldg(p.dst + pos);
+                } else {
+                    e1 = 0;
+                }
+            } else {
+                const uint2 e = __ldg((G.kind == ANCHOR_OUT ? p.out_ent : p.in_ent) + pos);
+                etr = e.x;
+                e1 = e.y;
+            }
+            if (STATS) st[ST_BATCHES]++;
+            if (etr > h || pos >= lim) {  // window end
+                ++g;
+                scan = false;
+                break;
+            }
+            ++pos;
+            if (etr <= tr_prev) break;  // before the window (lower-bound start)
+            if (STATS) {
+                st[ST_ENTRIES]++;
+                st[ST_BYTES] += glob ? 12 : 8;
+            }
+            uint32_t cls;
+            if (glob)
+                cls = (e1 != e2 && classify<MAXV>(m2g, e1) == CLS_NEW && classify<MAXV>(m2g, e2) == CLS_NEW)
+                          ? CLS_NEW : 0xFEu;
+            else
+                cls = classify<MAXV>(m2g, e1);
+            uint32_t hit = kNone;
+            for (uint32_t c = G.child_begin; c < G.child_end; ++c)
+                if (s_nodes[c].want == cls) {
+                    hit = c;
+                    break;
+                }
+            if (hit == kNone) break;
+            const LNode dn = s_nodes[hit];
+            if (dn.flags & NODE_COMPLETION) {
+                count_n(dn.slot, tid, 1);
+                if (STATS) st[ST_MATCHES]++;
+            }
+            if (dn.flags & NODE_INNER) {
+                myfr[(d * kFrameWords + 0) * kLB] = node | (g << 16);
+                myfr[(d * kFrameWords + 1) * kLB] = pos;
+                myfr[(d * kFrameWords + 2) * kLB] = tr_prev;
+                myfr[(d * kFrameWords + 3) * kLB] = lim;
+                myfr[(d * kFrameWords + 4) * kLB] = P.x;
+                myfr[(d * kFrameWords + 5) * kLB] = P.y;
+                myfr[(d * kFrameWords + 6) * kLB] = P.z;
+                myfr[(d * kFrameWords + 7) * kLB] = P.w;
+                ++d;
+                if (dn.n_new >= 1) m2g_set<MAXV>(m2g, nv, e1);
+                if (dn.n_new == 2) m2g_set<MAXV>(m2g, nv + 1, e2);
+                nv = dn.nv;
+                tr_prev = etr;
+                P = glob ? __ldg(p.eptr + (pos - 1))
+                         : __ldg((G.kind == ANCHOR_OUT ? p.out_ptr : p.in_ptr) + (pos - 1));
+                node = hit;
+                g = dn.group_begin;
+                g_end = dn.group_end;
+                lim = kNone;
+                scan = false;
+                fresh = true;
+                if (STATS) {
+                    st[ST_NODES]++;
+                    st[ST_BYTES] += 16;
+                }
+            }
+        } while (0);
+
+        // ---------------------------------------------------- warp cooperation
+        // (1) long leaf windows: the whole warp scans each parked window, 32 entries per
+        //     step, one ballot per leaf child, and credits the owning lane's counters.
+        unsigned hm = __ballot_sync(kFull, help);
+        while (hm) {
+            const int j = __ffs(hm) - 1;
+            hm &= hm - 1;
+            const uint32_t gj = __shfl_sync(kFull, g, j);
+            const uint32_t hj = __shfl_sync(kFull, h, j);
+            const uint32_t tpj = __shfl_sync(kFull, tr_prev, j);
+            const uint32_t nvj = __shfl_sync(kFull, nv, j);
+            uint32_t mj[MAXV];
+#pragma unroll
+            for (int k = 0; k < MAXV; k++) mj[k] = __shfl_sync(kFull, m2g[k], j);
+            const DGroup G = s_groups[gj];
+            const uint2 *ent = (G.kind == ANCHOR_OUT) ? p.out_ent : p.in_ent;
+            uint32_t b = __shfl_sync(kFull, pos, j);
+            for (;;) {
+                const uint2 e = __ldg(ent + b + lane);
+                const unsigned fm = __ballot_sync(kFull, e.x > hj);
+                const unsigned inmask = fm ? ((1u << (__ffs(fm) - 1)) - 1u) : kFull;
+                const bool w = ((inmask >> lane) & 1u) && e.x > tpj;
+                const uint32_t cls = classify<MAXV>(mj, e.y);
+                for (uint32_t c = G.child_begin; c < G.child_end; ++c) {
+                    const LNode dn = s_nodes[c];
+                    const unsigned mc = __ballot_sync(kFull, w && cls == dn.want);
+                    if (lane == 0 && mc && (dn.flags & NODE_COMPLETION)) count_n(dn.slot, wbase + j, __popc(mc));
+                    if (STATS && lane == 0) st[ST_MATCHES] += __popc(mc);
+                }
+                if (STATS) {
+                    const uint32_t we = __popc(__ballot_sync(kFull, w));
+                    if (lane == 0) {
+                        st[ST_ENTRIES] += we;
+                        st[ST_BYTES] += 8ull * we;
+                        st[ST_BATCHES]++;
+                    }
+                    n_help++;
+                }
+                if (fm) break;
+                b += 32;
+            }
+            if (lane == j) {
+                help = false;
+                scan = false;
+                ++g;
+            }
+        }
+        // (2) split heavy searches: a lane that has run for more than kAgeMin steps on one
+        //     root/task hands each partial match it descends into to this warp's task stack
+        //     (the paper's intra-warp balancing); any idle lane of the warp
+        //     mines that subtree only (its frame stack starts there) and the donor returns to
+        //     its parent's window.  Sibling exclusivity holds by
+        //     construction: a task is one partial match, handed over before any child of it
+        //     was examined.
+        {
+            const unsigned don = __ballot_sync(kFull, fresh && active && (age > kAgeMin || !roots_left));
+            const uint32_t n = min((uint32_t)__popc(don), kStackCap - stop);
+            if (n) {
+                const uint32_t rank = __popc(don & lt_mask);
+                if (((don >> lane) & 1u) && rank < n) {
+                    const uint32_t slot = stop + rank;
+                    wstk[0 * kStackCap + slot] = node | (nv << 16);
+                    wstk[1 * kStackCap + slot] = tr_prev;
+                    wstk[2 * kStackCap + slot] = h;
+                    wstk[3 * kStackCap + slot] = P.x;
+                    wstk[4 * kStackCap + slot] = P.y;
+                    wstk[5 * kStackCap + slot] = P.z;
+                    wstk[6 * kStackCap + slot] = P.w;
+                    wstk[7 * kStackCap + slot] = R.x;
+                    wstk[8 * kStackCap + slot] = R.y;
+                    wstk[9 * kStackCap + slot] = R.z;
+                    wstk[10 * kStackCap + slot] = R.w;
+#pragma unroll
+                    for (int q = 0; q < MAXV; q++) wstk[(11 + q) * kStackCap + slot] = m2g[q];
+                    g = g_end;  // handed out: pop back to the parent at the next step
+                    fresh = false;
+                    if (STATS) st[ST_OFFLOADS]++;
+                }
+                stop += n;
+            }
+        }
+
+        // ---------------------------------------------------- (3) termination
+        if (!roots_left && stop == 0 && !__any_sync(kFull, active)) break;
+    }
+
+    if (STATS && p.dbg && lane == 0) {
+        unsigned long long t_end, smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        uint32_t sm32;
+        asm("mov.u32 %0, %%smid;" : "=r"(sm32));
+        smid = sm32;
+        unsigned long long *r = p.dbg + (size_t)(blockIdx.x * (kLB / 32) + (tid >> 5)) * 8;
+        r[0] = t_start; r[1] = t_end; r[2] = n_iter; r[3] = n_help; r[4] = n_roots_w; r[5] = t_roots_done;
+        r[6] = smid; r[7] = 0;
+    }
+    // ---- counters: lanes -> block -> global, once per block
+    __syncthreads();
+    if (LANECNT) {
+        for (uint32_t s = (uint32_t)tid >> 5; s < p.n_slots; s += kLB / 32) {
+            unsigned long long v = 0;
+            for (int i = lane; i < kLB; i += 32) v += s_cnt[s * kLB + i];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+            if (lane == 0) s_tot[s] += v;
+        }
+        __syncthreads();
+    }
+    for (uint32_t i = tid; i < p.n_motifs; i += kLB) {
+        const unsigned long long v = s_tot[s_nodes[p.motif_node[i]].slot];
+        if (v) atomicAdd(p.counts + i, v);
+    }
+    if (STATS) {
+#pragma unroll
+        for (int i = 0; i < ST_N; i++) {
+            unsigned long long v = st[i];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+            if (lane == 0 && v) atomicAdd(p.stats + i, v);
+        }
+    }
+}
+
+}  // namespace lane

@@ -323,8 +323,9 @@ def main():
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": E / tt.item(), "unit": UNIT, "s_per_step": tt.item(),
-               "h2d_bytes_per_step": 36 * E + 8 * (V + 1), "d2h_bytes_per_step": 8 * k,
-               "path": "mayura_load_graph(host arrays: sort+CSR on host, H2D) + mayura_comine + D2H counts"}
+               "h2d_bytes_per_step": 16 * E, "d2h_bytes_per_step": 8 * k,
+               "path": "mayura_load_graph(pinned host src/dst/t -> H2D, graph build on the GPU) + "
+                       "mayura_comine + D2H of the counts"}
 
     cpu = None
     parity = None

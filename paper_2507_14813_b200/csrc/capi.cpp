@@ -37,6 +37,7 @@ extern "C" mayura_status mayura_graph_export(mayura_graph g, uint32_t *src, uint
                                              uint32_t *out_ent, uint32_t *in_off, uint32_t *in_ent) {
     clear_error();
     if (!g) return fail(MAYURA_E_INVALID, "mayura_graph_export: NULL handle");
+    if (mayura_status s = ensure_host(g)) return s;  // device-built graph: download once
     const size_t E = (size_t)g->E, V1 = (size_t)g->V + 1;
     if (src) std::memcpy(src, g->src.data(), 4 * E);
     if (dst) std::memcpy(dst, g->dst.data(), 4 * E);
@@ -53,6 +54,7 @@ extern "C" mayura_status mayura_graph_export(mayura_graph g, uint32_t *src, uint
 extern "C" mayura_status mayura_graph_export_succ(mayura_graph g, uint32_t *eptr) {
     clear_error();
     if (!g || !eptr) return fail(MAYURA_E_INVALID, "mayura_graph_export_succ: NULL argument");
+    if (mayura_status s = ensure_host(g)) return s;
     std::memcpy(eptr, g->eptr.data(), 4 * g->eptr.size());
     return MAYURA_OK;
 }
@@ -117,6 +119,7 @@ extern "C" mayura_status mayura_partition_roots(mayura_graph g, int64_t delta, u
     clear_error();
     if (!g || !bounds_out || n_parts == 0) return fail(MAYURA_E_INVALID, "mayura_partition_roots: bad argument");
     if (delta < 0) return fail(MAYURA_E_INVALID, "mayura_partition_roots: delta < 0");
+    if (mayura_status s = ensure_host(g)) return s;
     const uint64_t E = g->E;
     const std::vector<int64_t> &t = g->t;
     std::vector<uint64_t> pref(E + 1, 0);

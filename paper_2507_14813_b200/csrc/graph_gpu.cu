@@ -1,0 +1,345 @@
+// graph_gpu.cu -- step a0 on the device: the time-sorted edge arrays and per-vertex out/in
+// adjacency ("Data-Loading", §4.2: "CSR ... with edges sorted in
+// ascending order of timestamps"), built on the graph's GPU from the caller's host
+// arrays.  Same layout and results as the host builder (graph_build.cpp, used for
+// host-only graphs); tests/test_gpu_parity.py checks the two are identical array by array.
+//
+//   ids        stable radix sort of (t - t_min) with the input rank as value (CUB onesweep):
+//              edge id i = i-th edge in (t, input rank) order; perm[i] = its input rank
+//   tr[i]      first id with timestamp t[i] (binary search in the sorted t)
+//   out/in CSR stable radix sort of the source (destination) with the edge id as value,
+//              so every list is in edge-id (= time) order; list x occupies
+//              [off[x], off[x+1]-1) followed by one sentinel entry (tr = nbr = 0xFFFFFFFF)
+//   eptr[e]    successor pointers: first list position with time rank > tr[e] in
+//              out(src), in(dst), out(dst), in(src) (binary searches)
+//   *_ptr[p]   eptr of the edge behind each list entry (sentinels: 0)
+// Host copies are made lazily (ensure_host) only when an inspection call needs them.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+
+#include <mutex>
+#include <string>
+#include <type_traits>
+
+#include "internal.h"
+
+namespace mayura {
+namespace {
+
+mayura_status cfail(cudaError_t e, const char *what) {
+    return fail(MAYURA_E_CUDA, std::string("mayura_load_graph: ") + what + ": " + cudaGetErrorString(e));
+}
+#define GK(call, what)                                  \
+    do {                                                \
+        cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return cfail(e_, what);  \
+    } while (0)
+
+constexpr int kT = 256;
+
+inline uint32_t blocks_for(uint64_t n) { return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((n + kT - 1) / kT, 148u * 64u)); }
+
+int bits_for(uint64_t maxval) {
+    int b = 0;
+    while (b < 64 && (maxval >> b) != 0) b++;
+    return b;
+}
+
+__global__ void k_check_ids(const uint32_t *src, const uint32_t *dst, uint32_t E, uint32_t V, uint32_t *bad) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x)
+        if (src[i] >= V || dst[i] >= V) atomicOr(bad, 1u);
+}
+
+__global__ void k_iota_key(const int64_t *t, int64_t tmin, uint64_t *key, uint32_t *val, uint32_t E) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
+        key[i] = (uint64_t)t[i] - (uint64_t)tmin;
+        val[i] = i;
+    }
+}
+
+__global__ void k_gather(const uint32_t *perm, const uint32_t *isrc, const uint32_t *idst, const int64_t *it,
+                         uint32_t *src, uint32_t *dst, int64_t *t, uint32_t E) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
+        const uint32_t r = perm[i];
+        src[i] = isrc[r];
+        dst[i] = idst[r];
+        t[i] = it[r];
+    }
+}
+
+// tr[i] = first index with t == t[i] (t sorted)
+__global__ void k_time_rank(const int64_t *t, uint32_t *tr, uint32_t E) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
+        const int64_t x = t[i];
+        uint32_t lo = 0, hi = i;
+        while (lo < hi) {
+            const uint32_t m = lo + ((hi - lo) >> 1);
+            if (t[m] < x) lo = m + 1;
+            else hi = m;
+        }
+        tr[i] = lo;
+    }
+}
+
+__global__ void k_iota(uint32_t *v, uint32_t E) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) v[i] = i;
+}
+
+// off[x] = (number of edges whose key < x) + x   (one sentinel slot per earlier list)
+__global__ void k_offsets(const uint32_t *skey, uint32_t E, uint32_t V, uint32_t *off) {
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x <= V; x += gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = E;
+        while (lo < hi) {
+            const uint32_t m = lo + ((hi - lo) >> 1);
+            if (skey[m] < x) lo = m + 1;
+            else hi = m;
+        }
+        off[x] = lo + x;
+    }
+}
+
+// list entries in sorted (key, edge id) order; ids[pos] = edge id of list position pos
+__global__ void k_scatter(const uint32_t *skey, const uint32_t *seid, const uint32_t *tr, const uint32_t *nbr,
+                          uint32_t E, uint2 *ent, uint32_t *ids) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
+        const uint32_t e = seid[i];
+        const uint32_t pos = i + skey[i];
+        ent[pos] = make_uint2(tr[e], nbr[e]);
+        ids[pos] = e;
+    }
+}
+
+__device__ __forceinline__ uint32_t first_after(const uint32_t *off, const uint2 *ent, uint32_t x, uint32_t key) {
+    uint32_t lo = off[x], hi = off[x + 1] - 1;  // excludes the sentinel
+    while (lo < hi) {
+        const uint32_t m = lo + ((hi - lo) >> 1);
+        if (ent[m].x > key) hi = m;
+        else lo = m + 1;
+    }
+    return lo;
+}
+
+__global__ void k_succ(const uint32_t *src, const uint32_t *dst, const uint32_t *tr, const uint32_t *out_off,
+                       const uint2 *out_ent, const uint32_t *in_off, const uint2 *in_ent, uint32_t E, uint4 *eptr) {
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        const uint32_t a = src[e], b = dst[e], key = tr[e];
+        eptr[e] = make_uint4(first_after(out_off, out_ent, a, key), first_after(in_off, in_ent, b, key),
+                             first_after(out_off, out_ent, b, key), first_after(in_off, in_ent, a, key));
+    }
+}
+
+__global__ void k_entry_ptr(const uint32_t *ids, const uint4 *eptr, uint32_t N, uint4 *ptr) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
+        const uint32_t e = ids[p];
+        ptr[p] = e != 0xFFFFFFFFu ? eptr[e] : make_uint4(0, 0, 0, 0);
+    }
+}
+
+struct Tmp {  // scratch freed at scope exit
+    std::vector<void *> p;
+    template <typename T>
+    cudaError_t get(T *&x, size_t n) {
+        void *v = nullptr;
+        cudaError_t e = (cudaError_t)dmalloc(&v, n * sizeof(T));
+        if (e == cudaSuccess) p.push_back(v);
+        x = reinterpret_cast<T *>(v);
+        return e;
+    }
+    ~Tmp() {
+        for (void *v : p) dfree(v);
+    }
+};
+
+}  // namespace
+
+int dmalloc(void **p, size_t bytes) {
+    static std::mutex mu;
+    static bool pooled[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev >= 0 && dev < 64 && !pooled[dev]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t keep = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+            }
+            pooled[dev] = true;
+        }
+    }
+    return (int)cudaMallocAsync(p, bytes ? bytes : 1, 0);
+}
+
+void dfree(void *p) {
+    if (p) cudaFreeAsync(p, 0);
+}
+
+mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, const int64_t *ht, uint64_t E64,
+                                 uint32_t V, mayura_graph_s *g) {
+    if (E64 + (uint64_t)V + 64 > 0xFFFFFFFFull)
+        return fail(MAYURA_E_LIMIT, "mayura_load_graph: n_edges + n_vertices exceeds 32-bit list positions");
+    const uint32_t E = (uint32_t)E64;
+    const size_t N = (size_t)E + V;  // list positions incl. sentinels
+    g->E = E;
+    g->V = V;
+    g->host_built = false;
+    cudaStream_t s = nullptr;
+    uint64_t bytes = 0;
+    auto alloc = [&](auto *&d, size_t n, int fill) -> cudaError_t {
+        using T = std::remove_reference_t<decltype(*d)>;
+        cudaError_t e = (cudaError_t)dmalloc(reinterpret_cast<void **>(&d), (n ? n : 1) * sizeof(T));
+        if (e != cudaSuccess) return e;
+        bytes += (n ? n : 1) * sizeof(T);
+        return fill >= 0 ? cudaMemsetAsync(d, fill, (n ? n : 1) * sizeof(T), s) : cudaSuccess;
+    };
+    // product arrays (freed by free_device on error)
+    GK(alloc(g->d_src, E + kPadE, 0), "cudaMalloc(src)");
+    GK(alloc(g->d_dst, E + kPadE, 0), "cudaMalloc(dst)");
+    GK(alloc(g->d_tr, E + kPadE, 0xFF), "cudaMalloc(tr)");
+    GK(alloc(g->d_t, (size_t)E, -1), "cudaMalloc(t)");
+    GK(alloc(g->d_hi, E + kPadE, 0), "cudaMalloc(hi)");
+    GK(alloc(g->d_eptr, 4 * ((size_t)E + kPadE), 0), "cudaMalloc(eptr)");
+    GK(alloc(g->d_out_off, (size_t)V + 1, -1), "cudaMalloc(out_off)");
+    GK(alloc(g->d_in_off, (size_t)V + 1, -1), "cudaMalloc(in_off)");
+    GK(alloc(g->d_out_ent, 2 * (N + kPadEnt), 0xFF), "cudaMalloc(out_ent)");
+    GK(alloc(g->d_in_ent, 2 * (N + kPadEnt), 0xFF), "cudaMalloc(in_ent)");
+    GK(alloc(g->d_out_ptr, 4 * (N + kPadE), 0), "cudaMalloc(out_ptr)");
+    GK(alloc(g->d_in_ptr, 4 * (N + kPadE), 0), "cudaMalloc(in_ptr)");
+    GK(alloc(g->d_perm, (size_t)E, -1), "cudaMalloc(perm)");
+    g->device_bytes += bytes;
+
+    Tmp tmp;
+    uint32_t *isrc, *idst, *bad, *val, *val2, *skey, *ids[2];
+    int64_t *it;
+    uint64_t *key, *key2;
+    GK(tmp.get(isrc, E), "cudaMalloc(tmp)");
+    GK(tmp.get(idst, E), "cudaMalloc(tmp)");
+    GK(tmp.get(it, E), "cudaMalloc(tmp)");
+    GK(tmp.get(bad, 4), "cudaMalloc(tmp)");
+    GK(cudaMemcpyAsync(isrc, hsrc, 4ull * E, cudaMemcpyHostToDevice, s), "H2D(src)");
+    GK(cudaMemcpyAsync(idst, hdst, 4ull * E, cudaMemcpyHostToDevice, s), "H2D(dst)");
+    GK(cudaMemcpyAsync(it, ht, 8ull * E, cudaMemcpyHostToDevice, s), "H2D(t)");
+    GK(cudaMemsetAsync(bad, 0, 16, s), "memset");
+    if (E) k_check_ids<<<blocks_for(E), kT, 0, s>>>(isrc, idst, E, V, bad);
+    // time range -> key bits
+    int64_t *mm;
+    GK(tmp.get(mm, 2), "cudaMalloc(tmp)");
+    size_t tb = 0, tb2 = 0;
+    int64_t tmin = 0, tmax = 0;
+    if (E) {
+        GK(cub::DeviceReduce::Min(nullptr, tb, it, mm, (int)E, s), "cub Min");
+        GK(cub::DeviceReduce::Max(nullptr, tb2, it, mm + 1, (int)E, s), "cub Max");
+        tb = std::max(tb, tb2);
+        char *cr;
+        GK(tmp.get(cr, tb), "cudaMalloc(tmp)");
+        GK(cub::DeviceReduce::Min(cr, tb, it, mm, (int)E, s), "cub Min");
+        GK(cub::DeviceReduce::Max(cr, tb, it, mm + 1, (int)E, s), "cub Max");
+        int64_t hm[2];
+        uint32_t hbad = 0;
+        GK(cudaMemcpyAsync(hm, mm, 16, cudaMemcpyDeviceToHost, s), "D2H(minmax)");
+        GK(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s), "D2H(check)");
+        GK(cudaStreamSynchronize(s), "sync");
+        if (hbad) return fail(MAYURA_E_INVALID, "mayura_load_graph: vertex id >= n_vertices");
+        tmin = hm[0];
+        tmax = hm[1];
+    }
+    // 1. stable sort by (t, input rank)
+    GK(tmp.get(key, E), "cudaMalloc(tmp)");
+    GK(tmp.get(key2, E), "cudaMalloc(tmp)");
+    GK(tmp.get(val, E), "cudaMalloc(tmp)");
+    if (E) {
+        k_iota_key<<<blocks_for(E), kT, 0, s>>>(it, tmin, key, val, E);
+        const int tbits = std::max(1, bits_for((uint64_t)tmax - (uint64_t)tmin));
+        size_t need = 0;
+        GK(cub::DeviceRadixSort::SortPairs(nullptr, need, key, key2, val, g->d_perm, (int)E, 0, tbits, s), "cub sort");
+        char *ct;
+        GK(tmp.get(ct, need), "cudaMalloc(tmp)");
+        GK(cub::DeviceRadixSort::SortPairs(ct, need, key, key2, val, g->d_perm, (int)E, 0, tbits, s), "cub sort");
+        k_gather<<<blocks_for(E), kT, 0, s>>>(g->d_perm, isrc, idst, it, g->d_src, g->d_dst, g->d_t, E);
+        // 2. time ranks
+        k_time_rank<<<blocks_for(E), kT, 0, s>>>(g->d_t, g->d_tr, E);
+    }
+    // 3. out / in adjacency
+    GK(tmp.get(skey, E), "cudaMalloc(tmp)");
+    GK(tmp.get(val2, E), "cudaMalloc(tmp)");
+    GK(tmp.get(ids[0], N + 1), "cudaMalloc(tmp)");
+    GK(tmp.get(ids[1], N + 1), "cudaMalloc(tmp)");
+    const int vbits = std::max(1, bits_for(V ? V - 1 : 0));
+    for (int dir = 0; dir < 2; dir++) {
+        const uint32_t *k_in = dir == 0 ? g->d_src : g->d_dst;
+        const uint32_t *nbr = dir == 0 ? g->d_dst : g->d_src;
+        uint32_t *off = dir == 0 ? g->d_out_off : g->d_in_off;
+        uint2 *ent = reinterpret_cast<uint2 *>(dir == 0 ? g->d_out_ent : g->d_in_ent);
+        GK(cudaMemsetAsync(ids[dir], 0xFF, 4 * (N + 1), s), "memset(ids)");
+        if (E) {
+            k_iota<<<blocks_for(E), kT, 0, s>>>(val, E);
+            size_t need = 0;
+            GK(cub::DeviceRadixSort::SortPairs(nullptr, need, k_in, skey, val, val2, (int)E, 0, vbits, s), "cub sort");
+            char *ct;
+            GK(tmp.get(ct, need), "cudaMalloc(tmp)");
+            GK(cub::DeviceRadixSort::SortPairs(ct, need, k_in, skey, val, val2, (int)E, 0, vbits, s), "cub sort");
+            k_scatter<<<blocks_for(E), kT, 0, s>>>(skey, val2, g->d_tr, nbr, E, ent, ids[dir]);
+        }
+        k_offsets<<<blocks_for((uint64_t)V + 1), kT, 0, s>>>(skey, E, V, off);
+    }
+    // 4. successor pointers, then each list entry's copy of them
+    if (E)
+        k_succ<<<blocks_for(E), kT, 0, s>>>(g->d_src, g->d_dst, g->d_tr, g->d_out_off,
+                                            reinterpret_cast<const uint2 *>(g->d_out_ent), g->d_in_off,
+                                            reinterpret_cast<const uint2 *>(g->d_in_ent), E,
+                                            reinterpret_cast<uint4 *>(g->d_eptr));
+    if (N) {
+        k_entry_ptr<<<blocks_for(N), kT, 0, s>>>(ids[0], reinterpret_cast<const uint4 *>(g->d_eptr),
+                                                 (uint32_t)N, reinterpret_cast<uint4 *>(g->d_out_ptr));
+        k_entry_ptr<<<blocks_for(N), kT, 0, s>>>(ids[1], reinterpret_cast<const uint4 *>(g->d_eptr),
+                                                 (uint32_t)N, reinterpret_cast<uint4 *>(g->d_in_ptr));
+    }
+    GK(cudaGetLastError(), "graph build kernels");
+    GK(cudaStreamSynchronize(s), "graph build");
+    return MAYURA_OK;
+}
+
+// Host copies of a device-built graph, for the inspection / partitioning calls.
+mayura_status ensure_host(mayura_graph_s *g) {
+    if (g->host_built || g->device < 0) return MAYURA_OK;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(g->device);
+    const size_t E = g->E, V1 = (size_t)g->V + 1, N = (size_t)g->E + g->V;
+    try {
+        g->src.resize(E); g->dst.resize(E); g->tr.resize(E); g->t.resize(E); g->perm.resize(E);
+        g->out_off.resize(V1); g->in_off.resize(V1);
+        g->out_ent.resize(2 * N); g->in_ent.resize(2 * N);
+        g->eptr.resize(4 * E); g->out_ptr.resize(4 * N); g->in_ptr.resize(4 * N);
+    } catch (const std::bad_alloc &) {
+        cudaSetDevice(prev);
+        return fail(MAYURA_E_OOM, "ensure_host: out of host memory");
+    }
+    std::vector<uint32_t> perm32(E);
+    cudaError_t e = cudaSuccess;
+    auto cp = [&](void *h, const void *d, size_t b) {
+        if (e == cudaSuccess && b) e = cudaMemcpy(h, d, b, cudaMemcpyDeviceToHost);
+    };
+    cp(g->src.data(), g->d_src, 4 * E);
+    cp(g->dst.data(), g->d_dst, 4 * E);
+    cp(g->tr.data(), g->d_tr, 4 * E);
+    cp(g->t.data(), g->d_t, 8 * E);
+    cp(perm32.data(), g->d_perm, 4 * E);
+    cp(g->out_off.data(), g->d_out_off, 4 * V1);
+    cp(g->in_off.data(), g->d_in_off, 4 * V1);
+    cp(g->out_ent.data(), g->d_out_ent, 8 * N);
+    cp(g->in_ent.data(), g->d_in_ent, 8 * N);
+    cp(g->eptr.data(), g->d_eptr, 16 * E);
+    cp(g->out_ptr.data(), g->d_out_ptr, 16 * N);
+    cp(g->in_ptr.data(), g->d_in_ptr, 16 * N);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return fail(MAYURA_E_CUDA, std::string("ensure_host: ") + cudaGetErrorString(e));
+    for (size_t i = 0; i < E; i++) g->perm[i] = perm32[i];
+    g->host_built = true;
+    return MAYURA_OK;
+}
+
+}  // namespace mayura

@@ -67,6 +67,8 @@ struct mayura_graph_s {
     uint64_t E = 0;
     uint32_t V = 0;
     int device = -1;
+    bool host_built = true;                 // false: built on the GPU, host arrays made lazily
+    bool fresh_alloc = false;               // device scratch allocated since the last stream sync
     // host build results (edge id order)
     std::vector<uint32_t> src, dst, tr;
     std::vector<int64_t> t;
@@ -82,8 +84,7 @@ struct mayura_graph_s {
     uint32_t *d_out_off = nullptr, *d_in_off = nullptr;
     uint32_t *d_out_ent = nullptr, *d_in_ent = nullptr;  // uint2 {tr, nbr}
     uint32_t *d_eptr = nullptr, *d_out_ptr = nullptr, *d_in_ptr = nullptr;  // uint4
-    uint32_t *d_ctx = nullptr;                            // offloaded search contexts
-    uint32_t ctx_cap = 0, epoch = 0;
+    uint32_t *d_perm = nullptr;                           // input rank of edge id (GPU-built graphs)
     uint32_t *d_queue = nullptr;                         // work-queue cursors
     unsigned long long *d_counts = nullptr;              // scratch counts (host-output calls)
     uint32_t d_counts_cap = 0;
@@ -93,12 +94,6 @@ struct mayura_graph_s {
     uint32_t *d_bfs_ctl = nullptr, *d_bfs_long = nullptr;
     size_t bfs_bytes = 0;
     uint32_t bfs_seg_cap = 0, bfs_long_cap = 0;
-    uint32_t *d_wave = nullptr;                          // wave records + task lists + counters
-    size_t wave_bytes = 0, wave_pm_bytes = 0, wave_n_bytes = 0, wave_l_bytes = 0;
-    uint32_t wave_pm_seg = 0, wave_n_seg = 0, wave_l_seg = 0;
-    uint32_t *d_tile = nullptr;                          // tile task lists + counters
-    size_t tile_bytes = 0, tile_n_bytes = 0, tile_l_bytes = 0;
-    uint32_t tile_n_seg = 0, tile_l_seg = 0;
     uint64_t device_bytes = 0;
 };
 
@@ -118,6 +113,19 @@ struct mayura_mgtree_s {
 };
 
 namespace mayura {
+// device padding: 32 trailing elements after every per-edge / per-position array and 64
+// sentinel-valued entries after the adjacency, so batched and read-ahead loads never leave
+// the allocation
+constexpr size_t kPadE = 32, kPadEnt = 64;
+mayura_status build_graph_device(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t E,
+                                 uint32_t V, mayura_graph_s *g);
+mayura_status ensure_host(mayura_graph_s *g);
+// Library device memory comes from the device's stream-ordered pool with a retained release
+// threshold, so load / free / scratch-growth cycles reuse memory instead of paying
+// cudaMalloc / cudaFree (the e2e path builds and drops a graph per step).  dmalloc/dfree
+// order on the legacy default stream; callers synchronise before first use on another stream.
+int dmalloc(void **p, size_t bytes);  // cudaError_t as int (keeps this header CUDA-free)
+void dfree(void *p);
 mayura_status build_graph_host(const uint32_t *src, const uint32_t *dst, const int64_t *t,
                                uint64_t E, uint32_t V, mayura_graph_s *g);
 mayura_status compile_tree(const uint32_t *motif_edges, const uint32_t *motif_len,

@@ -226,3 +226,24 @@ def test_bfs_overflow_fallbacks(M, oracle_mod, monkeypatch):
     assert st["matches"] == sum(exp)
     if os.environ.get("MAYURA_KERNEL", "bfs") == "bfs":
         assert st["contexts"] > 0      # the depth-first fallback ran
+
+
+def test_gpu_graph_build_matches_host_builder(M):
+    """Step a0 on the GPU (CUB radix sorts + binary searches) produces exactly the arrays of
+    the host builder: edge order, time ranks, CSR offsets/entries/sentinels, successor pointers."""
+    cases = [synth.CONFIGS["C1"].graph(), synth.random_graph(11, 40, 5000, 300, self_loop_frac=0.05),
+             synth.out_star(1000), synth.random_graph(12, 3, 1, 5), ([], [], [], 4)]
+    big = synth.random_graph(13, 20, 2000, 50)
+    cases.append((big[0], big[1], big[2] + (1 << 40), big[3]))           # large timestamps
+    cases.append((big[0], big[1], big[2] - (1 << 40), big[3]))           # negative timestamps
+    for src, dst, t, V in cases:
+        eh = M.Graph(src, dst, t, V, device=-1).export()
+        ed = M.Graph(src, dst, t, V, device=0).export()
+        assert set(eh) == set(ed)
+        for key in eh:
+            assert np.array_equal(eh[key], ed[key]), key
+
+
+def test_gpu_graph_build_errors(M):
+    with pytest.raises(M.MayuraError):
+        M.Graph([0, 1], [1, 7], [0, 1], 3, device=0)     # vertex id >= n_vertices

@@ -28,6 +28,7 @@ namespace bfs {
 constexpr int kTB = 256;            // threads per block (expand pass)
 constexpr int kStripes = 64;        // output segments per level
 constexpr uint32_t kLong = 16;      // windows of >= kLong entries go to the warp pass
+constexpr int kTile = 4;            // entries loaded together at a window's start
 constexpr int kMaxLevels = MAYURA_MAX_EDGES;
 constexpr uint8_t NODE_PRELEAF = 8; // LNode flag: has children, all of them leaves
 
@@ -477,15 +478,19 @@ __global__ void __launch_bounds__(kTB) expand_kernel(const __grid_constant__ BPa
             uint32_t lim;
             const uint32_t start = window_start<MAXV, STATS>(p, G, x, lim, c);
             if (STATS) { c.st[ST_WINDOWS]++; c.st[ST_BYTES] += G.kind == ANCHOR_GLOBAL ? 12 : 8; }
-            // long window -> warp pass
+            // one round trip: the window's first kTile entries and the long-window probe
+            const bool glob = G.kind == ANCHOR_GLOBAL;
+            uint32_t etr[kTile], e1[kTile], e2[kTile];
+#pragma unroll
+            for (int k = 0; k < kTile; k++) load_entry(p, G, start + k, lim, etr[k], e1[k], e2[k]);
             bool is_long;
-            if (G.kind == ANCHOR_GLOBAL) {
+            if (glob) {
                 is_long = start + kLong <= x.h + 1;
             } else {
                 const uint2 *ent = (G.kind == ANCHOR_OUT) ? p.out_ent : p.in_ent;
                 is_long = __ldg(&ent[start + kLong - 1].x) <= x.h;
             }
-            if (is_long) {
+            if (is_long) {  // long window -> warp pass
                 const uint32_t li = atomicAdd(p.long_cnt, 1u);
                 if (li < p.long_cap) {
                     p.long_items[3 * (size_t)li + 0] = LEVEL0 ? x.root : item;
@@ -496,7 +501,41 @@ __global__ void __launch_bounds__(kTB) expand_kernel(const __grid_constant__ BPa
                 }
                 // no room: scan it here
             }
-            for (uint32_t pos = start;; ++pos) {
+            // the tile, unrolled: completions counted in place, inner matches collected
+            bool open = true;
+            unsigned inner = 0;
+            uint32_t ich[kTile];
+#pragma unroll
+            for (int k = 0; k < kTile; k++) {
+                open = open && !(etr[k] > x.h || start + k >= lim);
+                ich[k] = kNone;
+                if (open && etr[k] > x.tr_prev) {
+                    if (STATS) { c.st[ST_ENTRIES]++; c.st[ST_BYTES] += glob ? 12 : 8; }
+                    const uint32_t ch = find_child(s.nodes, G, entry_class<MAXV>(G, x.m2g, e1[k], e2[k]));
+                    if (ch != kNone) {
+                        const lane::LNode dn = s.nodes[ch];
+                        if (dn.flags & NODE_COMPLETION) {
+                            count_add(c, dn.slot, 1);
+                            if (STATS) c.st[ST_MATCHES]++;
+                        }
+                        if (dn.flags & NODE_INNER) {
+                            inner |= 1u << k;
+                            ich[k] = ch;
+                        }
+                    }
+                }
+            }
+            while (inner) {
+                const int k = __ffs(inner) - 1;
+                inner &= inner - 1;
+                uint32_t t_ = etr[0], a_ = e1[0], b_ = e2[0], ch = ich[0];
+#pragma unroll
+                for (int q = 1; q < kTile; q++)
+                    if (q == k) { t_ = etr[q]; a_ = e1[q]; b_ = e2[q]; ch = ich[q]; }
+                child<MAXV, STATS>(p, s.nodes, s.groups, G, s.nodes[ch], ch, x, start + k, t_, a_, b_, c);
+            }
+            if (!open) continue;
+            for (uint32_t pos = start + kTile;; ++pos) {  // windows longer than the tile
                 uint32_t etr, e1, e2;
                 load_entry(p, G, pos, lim, etr, e1, e2);
                 if (etr > x.h || pos >= lim) break;

@@ -78,6 +78,7 @@ struct DeviceTable {
     lane::LNode *lnodes;
     uint32_t *gwant;
     uint32_t n_nodes, n_groups, n_motifs, max_vertices, max_edges, n_slots;
+    bool generic;  // some anchor group searches its list or scans the edge array
 };
 
 // per group: wants of its first 4 children packed in bytes (0xFD: no child), for the
@@ -126,9 +127,9 @@ mayura_status cuda_fail(cudaError_t e, const char *what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, what); \
     } while (0)
 
-template <int MAXV, bool LANECNT, bool STATS>
+template <int MAXV, bool LANECNT, bool STATS, bool GEN>
 cudaError_t launch_lane_t(const lane::LParams &p, size_t smem, cudaStream_t s, int sms) {
-    auto kern = lane::comine_lane_kernel<MAXV, LANECNT, STATS>;
+    auto kern = lane::comine_lane_kernel<MAXV, LANECNT, STATS, GEN>;
     static std::mutex mu;
     static size_t cached_smem = 0;
     static int cached_dev = -1, cached_per_sm = 0;
@@ -160,19 +161,25 @@ cudaError_t launch_lane_t(const lane::LParams &p, size_t smem, cudaStream_t s, i
 constexpr size_t kLaneCntSmem = 48 * 1024;  // lane-private counters while they fit this budget
 
 template <int MAXV>
-cudaError_t launch_lane_v(const lane::LParams &p, bool stats, cudaStream_t s, int sms) {
+cudaError_t launch_lane_v(const lane::LParams &p, bool stats, bool generic, cudaStream_t s, int sms) {
     const bool lanecnt = (size_t)p.n_slots * lane::kLB * 4 <= kLaneCntSmem;
     const size_t smem = lane::smem_total(p.n_nodes, p.n_groups, p.n_slots, p.n_frames, lanecnt, MAXV);
+    if (stats)  // the instrumented kernel is always the generic one
+        return lanecnt ? launch_lane_t<MAXV, true, true, true>(p, smem, s, sms)
+                       : launch_lane_t<MAXV, false, true, true>(p, smem, s, sms);
     if (lanecnt)
-        return stats ? launch_lane_t<MAXV, true, true>(p, smem, s, sms) : launch_lane_t<MAXV, true, false>(p, smem, s, sms);
-    return stats ? launch_lane_t<MAXV, false, true>(p, smem, s, sms) : launch_lane_t<MAXV, false, false>(p, smem, s, sms);
+        return generic ? launch_lane_t<MAXV, true, false, true>(p, smem, s, sms)
+                       : launch_lane_t<MAXV, true, false, false>(p, smem, s, sms);
+    return generic ? launch_lane_t<MAXV, false, false, true>(p, smem, s, sms)
+                   : launch_lane_t<MAXV, false, false, false>(p, smem, s, sms);
 }
 
-cudaError_t launch_lane(const lane::LParams &p, uint32_t max_vertices, bool stats, cudaStream_t s, int sms) {
-    if (max_vertices <= 4) return launch_lane_v<4>(p, stats, s, sms);
-    if (max_vertices <= 6) return launch_lane_v<6>(p, stats, s, sms);
-    if (max_vertices <= 8) return launch_lane_v<8>(p, stats, s, sms);
-    return launch_lane_v<16>(p, stats, s, sms);
+cudaError_t launch_lane(const lane::LParams &p, uint32_t max_vertices, bool stats, bool generic, cudaStream_t s,
+                        int sms) {
+    if (max_vertices <= 4) return launch_lane_v<4>(p, stats, generic, s, sms);
+    if (max_vertices <= 6) return launch_lane_v<6>(p, stats, generic, s, sms);
+    if (max_vertices <= 8) return launch_lane_v<8>(p, stats, generic, s, sms);
+    return launch_lane_v<16>(p, stats, generic, s, sms);
 }
 
 // Kernel choice (MAYURA_KERNEL): "hybrid" (default), "lane", "bfs".
@@ -297,6 +304,8 @@ void table_view(const Table &t, uint32_t n_motifs, char *buf, DeviceTable &d) {
     d.max_edges = t.max_edges;
     d.n_slots = 0;
     for (const DNode &x : t.nodes) d.n_slots += (x.flags & NODE_COMPLETION) ? 1 : 0;
+    d.generic = false;
+    for (const DGroup &x : t.groups) d.generic = d.generic || x.kind == ANCHOR_GLOBAL || x.start == START_SEARCH;
 }
 
 mayura_status upload_table(const Table &t, uint32_t n_motifs, DeviceTable &d, void *&owner) {
@@ -388,7 +397,7 @@ lane::LParams lane_params(const mayura_graph_s *g, const DeviceTable &dt, uint32
     q.in_ent = reinterpret_cast<const uint2 *>(g->d_in_ent);
     q.out_ptr = reinterpret_cast<const uint4 *>(g->d_out_ptr);
     q.in_ptr = reinterpret_cast<const uint4 *>(g->d_in_ptr);
-    q.nodes = dt.lnodes; q.groups = dt.groups; q.motif_node = dt.motif_node;
+    q.nodes = dt.lnodes; q.groups = dt.groups; q.motif_node = dt.motif_node; q.gwant = dt.gwant;
     q.n_nodes = dt.n_nodes; q.n_groups = dt.n_groups; q.n_motifs = dt.n_motifs; q.n_slots = dt.n_slots;
     q.n_frames = dt.max_edges > 2 ? dt.max_edges - 2 : 0;
     q.r0 = r0; q.n_roots = n_roots; q.lb = lb; q.counts = counts; q.stats = stats;
@@ -441,7 +450,7 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         q.pm_seg_cap = g->bfs_seg_cap;
         q.pm_words = words;
     }
-    CK(launch_lane(q, dt.max_vertices, st, s, sms), "comine_lane_kernel launch");
+    CK(launch_lane(q, dt.max_vertices, st, dt.generic, s, sms), "comine_lane_kernel launch");
     return MAYURA_OK;
 }
 

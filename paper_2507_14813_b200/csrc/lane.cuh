@@ -33,6 +33,7 @@ constexpr uint32_t kHelpMin = 12;       // leaf windows of >= this many entries 
 constexpr uint32_t kAgeMin = 64;        // steps on one search before its descents are handed out
 constexpr uint32_t kStackCap = 32;      // per-warp task stack (tasks)
 constexpr int kPmStripes = 64;          // segments of a partial-match source (bfs::kStripes)
+constexpr uint32_t kGwMax = 64;         // groups whose packed child wants are kept in shared memory
 
 struct __align__(4) LNode {  // 12 bytes
     uint8_t want, n_new, nv, flags;
@@ -50,6 +51,7 @@ struct LParams {
     const LNode *nodes;
     const DGroup *groups;
     const uint32_t *motif_node;
+    const uint32_t *gwant;              // per group: wants of its first 4 children (bytes, 0xFD pad)
     uint32_t n_nodes, n_groups, n_motifs, n_slots, n_frames;
     uint32_t r0, n_roots;
     uint32_t *lb;                       // load-balancer words (LB_*), zeroed per launch
@@ -113,7 +115,9 @@ __device__ __forceinline__ uint32_t pick4(const uint4 &v, uint32_t k) {
     return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
 }
 
-template <int MAXV, bool LANECNT, bool STATS>
+// GEN: the tree has anchor groups that need a search (START_SEARCH) or scan the edge array
+// (GLOBAL); trees without them compile those paths out.
+template <int MAXV, bool LANECNT, bool STATS, bool GEN>
 __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_constant__ LParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     LNode *s_nodes = reinterpret_cast<LNode *>(smem);
@@ -123,6 +127,8 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
     uint32_t *s_fr = reinterpret_cast<uint32_t *>(smem + off_frames(p.n_nodes, p.n_groups, p.n_slots, LANECNT));
     uint32_t *s_stk = s_fr + (size_t)(p.n_frames ? p.n_frames : 1) * kFrameWords * kLB;
     __shared__ uint32_t s_pref[kPmStripes + 1];
+    __shared__ uint32_t s_gw[kGwMax];  // packed child wants (trees of <= kGwMax groups)
+    for (uint32_t i = threadIdx.x; i < p.n_groups && i < kGwMax; i += kLB) s_gw[i] = p.gwant[i];
     if (p.pm && threadIdx.x == 0) {
         uint32_t acc = 0;
         for (int i = 0; i < kPmStripes; i++) {
@@ -345,7 +351,7 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                     } else if (G.start < START_SEARCH) {
                         pos = pick4(R, G.start - START_R0);
                         lim = kNone;
-                    } else if (G.start == START_SEARCH) {
+                    } else if (GEN && G.start == START_SEARCH) {
                         const uint32_t x = m2g_get<MAXV>(m2g, G.anchor);
                         const uint32_t *off = (G.kind == ANCHOR_OUT) ? p.out_off : p.in_off;
                         const uint2 *ent = (G.kind == ANCHOR_OUT) ? p.out_ent : p.in_ent;
@@ -359,7 +365,7 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                         pos = lo;
                         lim = kNone;
                         if (STATS) st[ST_BYTES] += 8;
-                    } else {  // GLOBAL: edge ids after the tie group of the previous edge, up to hi(root)
+                    } else if (GEN) {  // GLOBAL: edge ids after the tie group of the previous edge, up to hi(root)
                         uint32_t lo = tr_prev, hi2 = h + 1;
                         while (lo < hi2) {
                             const uint32_t mid = lo + ((hi2 - lo) >> 1);
@@ -389,7 +395,7 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
             // scan one entry of the current window
             const DGroup G = s_groups[g];
             uint32_t etr, e1, e2 = 0;
-            const bool glob = G.kind == ANCHOR_GLOBAL;
+            const bool glob = GEN && G.kind == ANCHOR_GLOBAL;
             if (glob) {
                 etr = pos < lim ? __ldg(p.tr + pos) : kNone;
                 if (etr != kNone) {
@@ -422,11 +428,16 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
             else
                 cls = classify<MAXV>(m2g, e1);
             uint32_t hit = kNone;
-            for (uint32_t c = G.child_begin; c < G.child_end; ++c)
-                if (s_nodes[c].want == cls) {
-                    hit = c;
-                    break;
-                }
+            if (G.child_end - G.child_begin <= 4 && g < kGwMax) {  // one SIMD byte compare
+                const uint32_t eq = __vcmpeq4(s_gw[g], cls * 0x01010101u);
+                hit = eq ? G.child_begin + ((__ffs(eq) - 1) >> 3) : kNone;
+            } else {
+                for (uint32_t c = G.child_begin; c < G.child_end; ++c)
+                    if (s_nodes[c].want == cls) {
+                        hit = c;
+                        break;
+                    }
+            }
             if (hit == kNone) break;
             const LNode dn = s_nodes[hit];
             if (dn.flags & NODE_COMPLETION) {

@@ -19,7 +19,7 @@ for C in $CONFIGS; do
     --log-file gpurun_out/launches_${C}_${TAG}.csv python bench.py --config $C --profile --steps 3 --warmup 3 \
     > /dev/null 2>&1
   echo "ncu launches $C rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:comine_kernel -s 3 -c 1 \
-    -o gpurun_out/prof_${C}_${TAG} -f python bench.py --config $C --profile --steps 1 --warmup 4 > /dev/null 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"expand_kernel|long_kernel|comine_lane" \
+    -s 3 -c 3 -o gpurun_out/prof_${C}_${TAG} -f python bench.py --config $C --profile --steps 1 --warmup 4 > /dev/null 2>&1
   echo "ncu full $C rc=$?"
 done

@@ -110,6 +110,22 @@ def main():
                     if k in d:
                         lines.append("| %s (`%s`) | %s %s |" % (name, k, d[k], u.get(k, "")))
                 lines.append("")
+            # DRAM traffic of one co-mining pass (all captured kernels of one step) for bench.py
+            recs = ncu_raw(rp)
+            if recs:
+                tot = 0.0
+                names = []
+                for d, u in recs:
+                    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                        v = float(d.get(k, "0").replace(",", "") or 0)
+                        tot += v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u.get(k, "byte"), 1)
+                    names.append(d.get("Kernel Name", "?")[:80])
+                tj = os.path.join(PROF, "ncu_traffic.json")
+                allt = json.load(open(tj)) if os.path.exists(tj) else {}
+                allt[c] = {"dram_bytes_per_launch": tot, "kernels": names, "tag": tag,
+                           "note": "dram__bytes_read.sum + dram__bytes_write.sum summed over the kernels of one "
+                                   "co-mining pass, ncu --set full (cold L2 per replay)"}
+                json.dump(allt, open(tj, "w"), indent=1)
         with open(os.path.join(PROF, "%s_%s.md" % (tag, c)), "w") as f:
             f.write("\n".join(lines) + "\n")
         print("wrote profiles/%s_%s.md" % (tag, c))

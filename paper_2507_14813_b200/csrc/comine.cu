@@ -259,28 +259,48 @@ uint32_t rec_words(uint32_t max_vertices) {
 
 // Frontier / long-item / control buffers of the BFS passes, allocated once per graph and
 // grown on demand.  Capacity: 4 records per edge (>= 2^20, <= 2^26) per buffer.
-mayura_status ensure_bfs_buffers(mayura_graph_s *g, uint32_t words) {
-    const uint64_t recs = std::min<uint64_t>(std::max<uint64_t>(8 * g->E, 1u << 20), 1u << 26);
+// Frontier buffers of the breadth-first levels (nbufs = 1 for the hybrid's single level, 2 to
+// ping-pong), allocated per graph from the retained pool and grown on demand.  Capacity: 16
+// records per edge, at most 2^32 - 1 records and at most 40 % of the free device memory (a
+// full segment is still exact: that subtree is mined depth-first in place).  Long-window items:
+// 1 per edge (>= 2^20).
+mayura_status ensure_bfs_buffers(mayura_graph_s *g, uint32_t words, int nbufs) {
+    const size_t rb = (size_t)words * 4;
+    if (g->bfs_bytes && g->bfs_nbufs >= nbufs && g->bfs_words >= words && !getenv("MAYURA_BFS_SEG_CAP")) {
+        // sized once per graph (the query path must not pay cudaMemGetInfo)
+        g->bfs_seg_cap = (uint32_t)std::min<size_t>(g->bfs_bytes / ((size_t)bfs::kStripes * rb), 0xFFFFFFFFu);
+        return MAYURA_OK;
+    }
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t rec_bytes = (size_t)words * 4;
+    const uint64_t by_mem = (uint64_t)((free_b + (size_t)nbufs * g->bfs_bytes) * 0.4) / (rec_bytes * nbufs);
+    const uint64_t recs = std::max<uint64_t>(1u << 20, std::min<uint64_t>({16 * g->E, by_mem, 0xFFFFFFFFull}));
     uint32_t seg_cap = (uint32_t)((recs + bfs::kStripes - 1) / bfs::kStripes);
     // test hook: tiny capacities force the depth-first fallback / in-place long windows
     if (const char *e = getenv("MAYURA_BFS_SEG_CAP")) seg_cap = (uint32_t)std::max(1L, atol(e));
-    const size_t bytes = (size_t)seg_cap * bfs::kStripes * words * 4;
-    if (g->bfs_bytes < bytes) {
+    const size_t bytes = (size_t)seg_cap * bfs::kStripes * rec_bytes;
+    if (g->bfs_bytes < bytes || (nbufs == 2 && !g->d_bfs[1])) {
+        const size_t want = std::max(bytes, g->bfs_bytes);
         for (int i = 0; i < 2; i++)
             if (g->d_bfs[i]) dfree(g->d_bfs[i]), g->d_bfs[i] = nullptr;
-        g->device_bytes -= 2 * g->bfs_bytes;
+        g->device_bytes -= g->bfs_nbufs * g->bfs_bytes;
         g->bfs_bytes = 0;
-        for (int i = 0; i < 2; i++) CK((cudaError_t)dmalloc((void **)&g->d_bfs[i], bytes), "cudaMalloc(frontier)");
+        g->bfs_nbufs = 0;
+        for (int i = 0; i < nbufs; i++)
+            CK((cudaError_t)dmalloc((void **)&g->d_bfs[i], want), "cudaMalloc(frontier)");
         g->fresh_alloc = true;
-        g->bfs_bytes = bytes;
-        g->device_bytes += 2 * bytes;
+        g->bfs_bytes = want;
+        g->bfs_nbufs = nbufs;
+        g->bfs_words = std::max(g->bfs_words, words);
+        g->device_bytes += nbufs * want;
     }
-    g->bfs_seg_cap = std::min(seg_cap, (uint32_t)(g->bfs_bytes / ((size_t)bfs::kStripes * words * 4)));
+    g->bfs_seg_cap = std::min(seg_cap, (uint32_t)(g->bfs_bytes / ((size_t)bfs::kStripes * rec_bytes)));
     if (!g->d_bfs_ctl) {
         CK((cudaError_t)dmalloc((void **)&g->d_bfs_ctl, sizeof(uint32_t) * (kCtlWords * bfs::kMaxLevels + 16)),
            "cudaMalloc(bfs ctl)");
         g->fresh_alloc = true;
-        g->bfs_long_cap = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(g->E / 2, 1u << 20), 1u << 26);
+        g->bfs_long_cap = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(g->E, 1u << 20), 1u << 28);
         if (const char *e = getenv("MAYURA_BFS_LONG_CAP")) g->bfs_long_cap = (uint32_t)std::max(1L, atol(e));
         CK((cudaError_t)dmalloc((void **)&g->d_bfs_long, sizeof(uint32_t) * 3 * (size_t)g->bfs_long_cap),
            "cudaMalloc(long items)");
@@ -437,7 +457,7 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
     if (kind == K_BFS) levels = dt.max_edges > 1 ? dt.max_edges - 1 : 1;
     lane::LParams q = lane_params(g, dt, r0, n_roots, lb, counts, stats, st);
     if (levels > 0) {
-        mayura_status bs = ensure_bfs_buffers(g, words);
+        mayura_status bs = ensure_bfs_buffers(g, words, levels >= 2 ? 2 : 1);
         if (bs != MAYURA_OK) return bs;
         uint32_t *ctl = g->d_bfs_ctl;
         CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * (kCtlWords * bfs::kMaxLevels + 16), s), "cudaMemsetAsync(ctl)");
@@ -512,7 +532,8 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
         uint32_t mv = tabs[0].max_vertices;
         for (size_t i = 1; i < tabs.size(); i++) mv = std::max(mv, tabs[i].max_vertices);
         if (kernel_kind() != K_LANE && n_roots > 0) {
-            st = ensure_bfs_buffers(g, rec_words(mv));
+            const uint32_t lv = kernel_kind() == K_BFS ? 2u : std::min(hybrid_levels(), 2u);
+            if (lv > 0) st = ensure_bfs_buffers(g, rec_words(mv), lv >= 2 ? 2 : 1);
             if (st != MAYURA_OK) return st;
         }
         if (g->fresh_alloc) {

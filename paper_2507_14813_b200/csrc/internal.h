@@ -93,6 +93,8 @@ struct mayura_graph_s {
     uint32_t *d_bfs[2] = {nullptr, nullptr};             // BFS frontier buffers (ping-pong)
     uint32_t *d_bfs_ctl = nullptr, *d_bfs_long = nullptr;
     size_t bfs_bytes = 0;
+    int bfs_nbufs = 0;
+    uint32_t bfs_words = 0;
     uint32_t bfs_seg_cap = 0, bfs_long_cap = 0;
     uint64_t device_bytes = 0;
 };

@@ -284,8 +284,12 @@ CONFIGS: Dict[str, Config] = {
     "C3": Config("C3", "wiki-talk-temporal-shaped 1.14M nodes / 7.83M edges, delta=3600s, 12 motifs",
                  1_140_149, 7_833_140, int(6.24 * 365 * DAY), 3600, tuple(GROUP_C3), 2.1, 0.45,
                  120.0, 3, burst_frac=0.2, burst_width=1800.0, n_bursts=20000),
+    # alpha calibrated (SURVEY.md §8(d) calibration rule: tune the generator, not delta): at
+    # alpha = 2.1 the top vertex takes ~2.4 % of all edges (~550 per day), and 4-edge stars
+    # at delta = 1 day give ~1e6 matches per root; alpha = 2.5 gives a top vertex of ~31 edges
+    # per day (the SNAP stackoverflow-temporal order of magnitude) and ~60 matches per root.
     "C4": Config("C4", "stackoverflow-temporal-shaped 2.6M nodes / 63.5M edges, delta=86400s, 16 motifs",
-                 2_601_977, 63_497_050, int(7.6 * 365 * DAY), 86400, tuple(GROUP_C4), 2.1, 0.40,
+                 2_601_977, 63_497_050, int(7.6 * 365 * DAY), 86400, tuple(GROUP_C4), 2.5, 0.40,
                  600.0, 4),
     "C5": Config("C5", "transaction-graph-shaped (AML) 10M nodes / 500M edges, delta=3600s, 8 motifs",
                  10_000_000, 500_000_000, int(3.58 * 365 * DAY), 3600, tuple(GROUP_C5), 2.0, 0.40,

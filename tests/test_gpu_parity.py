@@ -247,3 +247,25 @@ def test_gpu_graph_build_matches_host_builder(M):
 def test_gpu_graph_build_errors(M):
     with pytest.raises(M.MayuraError):
         M.Graph([0, 1], [1, 7], [0, 1], 3, device=0)     # vertex id >= n_vertices
+
+
+@pytest.mark.slow
+def test_config_c4_sampled_parity(M, oracle_mod):
+    """C4 (63.5 M edges, delta = 1 day, 16 motifs up to 5 edges): the whole graph is mined on
+    the GPU; exact parity on sampled root ranges (the oracle cannot finish C4 in full,
+    SURVEY.md §8(d)); co-mined == independent on a sample; range additivity at full size."""
+    cfg = synth.CONFIGS["C4"]
+    src, dst, t, V = cfg.graph()
+    g = M.Graph(src, dst, t, V, device=0)
+    tree = M.MGTree(cfg.group(), cfg.delta)
+    E = g.n_edges
+    full = M.comine(g, tree)
+    assert all(x >= 0 for x in full) and sum(full) > 0
+    for a in (E // 3, (7 * E) // 10):
+        rng = (a, a + 1500)
+        exp = oracle_mod.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=rng)
+        assert M.comine(g, tree, rng) == exp
+        assert M.mine_independent(g, tree, rng) == exp
+    cut = E // 2
+    halves = [M.comine(g, tree, (0, cut)), M.comine(g, tree, (cut, E))]
+    assert [x + y for x, y in zip(*halves)] == full

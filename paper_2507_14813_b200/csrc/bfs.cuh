@@ -60,6 +60,9 @@ struct BParams {
     uint32_t long_cap;
     uint32_t *fallback;    // [0] subtrees mined depth-first because a segment was full
     uint32_t inline_preleaf;  // 1: count short pre-leaf windows inline (v4); 0: emit every inner child
+    uint32_t heavy_min;       // level 0 of the hybrid: a root is split breadth-first only if one of its
+                              // windows has >= heavy_min entries; lighter roots are handed to the
+                              // depth-first kernel whole, as a root record (0: split every root)
     unsigned long long *counts;
     unsigned long long *stats;
 };
@@ -77,7 +80,10 @@ struct Ctx {  // per-thread counters + stats
     uint32_t stride;
     unsigned long long *tot;
     unsigned long long st[ST_N];
+    uint32_t em_next, em_end;  // this thread's reserved run of output slots (chunked appends)
 };
+constexpr uint32_t kChunk = 8;     // output slots a thread reserves at once (expand pass)
+constexpr uint32_t kHole = 0xFFFFu; // node id of an unused reserved slot (skipped by readers)
 
 __device__ __forceinline__ void count_add(Ctx &c, uint32_t slot, uint32_t n) {
     uint32_t *q = c.cnt + slot * c.stride;
@@ -238,19 +244,36 @@ __device__ __noinline__ void dfs(const BParams &p, const lane::LNode *nodes, con
     }
 }
 
-// Append y to the next frontier (segment chosen by warp), else mine it here.
-template <int MAXV, bool STATS>
+__device__ __forceinline__ uint32_t out_seg() {
+    return ((blockIdx.x * (blockDim.x >> 5)) + (threadIdx.x >> 5)) % kStripes;
+}
+
+// Append y to the next frontier, else mine it here.  CHUNK (thread-per-item passes): the
+// thread reserves kChunk slots per atomic -- lanes reach this point divergently, so a
+// per-call warp-aggregated atomic would serialise one global round trip per lane; leftover
+// slots become holes (node kHole) written by close_chunk.  !CHUNK (warp passes, converged
+// lanes): one aggregated atomic per call.
+template <int MAXV, bool STATS, bool CHUNK = false>
 __device__ __forceinline__ void emit(const BParams &p, const lane::LNode *nodes, const DGroup *groups,
                                      const PM<MAXV> &y, Ctx &c) {
     constexpr int W = Rec<MAXV>::W;
-    const unsigned am = __activemask();
-    const int lane_id = threadIdx.x & 31;
-    const int leader = __ffs(am) - 1;
-    const uint32_t seg = ((blockIdx.x * (blockDim.x >> 5)) + (threadIdx.x >> 5)) % kStripes;
-    uint32_t base = 0;
-    if (lane_id == leader) base = atomicAdd(p.out.cnt + seg, (uint32_t)__popc(am));
-    base = __shfl_sync(am, base, leader);
-    const uint32_t idx = base + __popc(am & ((1u << lane_id) - 1u));
+    const uint32_t seg = out_seg();
+    uint32_t idx;
+    if (CHUNK) {
+        if (c.em_next == c.em_end) {
+            c.em_next = atomicAdd(p.out.cnt + seg, kChunk);
+            c.em_end = c.em_next + kChunk;
+        }
+        idx = c.em_next++;
+    } else {
+        const unsigned am = __activemask();
+        const int lane_id = threadIdx.x & 31;
+        const int leader = __ffs(am) - 1;
+        uint32_t base = 0;
+        if (lane_id == leader) base = atomicAdd(p.out.cnt + seg, (uint32_t)__popc(am));
+        base = __shfl_sync(am, base, leader);
+        idx = base + __popc(am & ((1u << lane_id) - 1u));
+    }
     if (idx < p.out.seg_cap) {
         uint4 *r = reinterpret_cast<uint4 *>(p.out.data + ((size_t)seg * p.out.seg_cap + idx) * W);
         r[0] = make_uint4(y.node | (y.nv << 16), y.root, y.tr_prev, y.h);
@@ -270,9 +293,19 @@ __device__ __forceinline__ void emit(const BParams &p, const lane::LNode *nodes,
     }
 }
 
+// Mark the unused rest of this thread's reserved run as holes.
+template <int MAXV>
+__device__ __forceinline__ void close_chunk(const BParams &p, Ctx &c) {
+    constexpr int W = Rec<MAXV>::W;
+    const uint32_t seg = out_seg();
+    for (uint32_t i = c.em_next; i < c.em_end && i < p.out.seg_cap; i++)
+        p.out.data[((size_t)seg * p.out.seg_cap + i) * W] = kHole;
+    c.em_next = c.em_end = 0;
+}
+
 // A matched inner child: count a pre-leaf child's leaf windows inline when they are
 // short, else hand the child to the next level.
-template <int MAXV, bool STATS>
+template <int MAXV, bool STATS, bool CHUNK>
 __device__ __forceinline__ void child(const BParams &p, const lane::LNode *nodes, const DGroup *groups,
                                       const DGroup &G, const lane::LNode &dn, uint32_t ch, const PM<MAXV> &x,
                                       uint32_t pos, uint32_t etr, uint32_t e1, uint32_t e2, Ctx &c) {
@@ -319,7 +352,7 @@ __device__ __forceinline__ void child(const BParams &p, const lane::LNode *nodes
             return;
         }
     }
-    emit<MAXV, STATS>(p, nodes, groups, y, c);
+    emit<MAXV, STATS, CHUNK>(p, nodes, groups, y, c);
 }
 
 // Read frontier record `item` (global index over the input segments, prefix in smem).
@@ -451,6 +484,7 @@ __global__ void __launch_bounds__(kTB) expand_kernel(const __grid_constant__ BPa
     c.tot = s.tot;
 #pragma unroll
     for (int i = 0; i < ST_N; i++) c.st[i] = 0;
+    c.em_next = c.em_end = 0;
     const uint32_t n_items = LEVEL0 ? p.n_roots : s.pref[kStripes];
     const lane::LNode root = s.nodes[0];
     for (uint32_t item = blockIdx.x * blockDim.x + threadIdx.x; item < n_items; item += gridDim.x * blockDim.x) {
@@ -469,8 +503,12 @@ __global__ void __launch_bounds__(kTB) expand_kernel(const __grid_constant__ BPa
                 if (root.flags & NODE_INNER) c.st[ST_NODES]++;
             }
             if (!(root.flags & NODE_INNER)) continue;
+            if (p.heavy_min && !lane::heavy_root<MAXV>(s.nodes, s.groups, root, x.P, x.h, p.out_ent, p.in_ent,
+                                                        p.heavy_min))
+                continue;  // light root: the depth-first kernel takes it from the root range
         } else {
             load_rec<MAXV>(p, s.pref, item, x);
+            if (x.node == kHole) continue;
         }
         const lane::LNode xn = s.nodes[x.node];
         for (uint32_t g = xn.group_begin; g < xn.group_end; ++g) {
@@ -532,7 +570,7 @@ __global__ void __launch_bounds__(kTB) expand_kernel(const __grid_constant__ BPa
 #pragma unroll
                 for (int q = 1; q < kTile; q++)
                     if (q == k) { t_ = etr[q]; a_ = e1[q]; b_ = e2[q]; ch = ich[q]; }
-                child<MAXV, STATS>(p, s.nodes, s.groups, G, s.nodes[ch], ch, x, start + k, t_, a_, b_, c);
+                child<MAXV, STATS, true>(p, s.nodes, s.groups, G, s.nodes[ch], ch, x, start + k, t_, a_, b_, c);
             }
             if (!open) continue;
             for (uint32_t pos = start + kTile;; ++pos) {  // windows longer than the tile
@@ -548,10 +586,11 @@ __global__ void __launch_bounds__(kTB) expand_kernel(const __grid_constant__ BPa
                     count_add(c, dn.slot, 1);
                     if (STATS) c.st[ST_MATCHES]++;
                 }
-                if (dn.flags & NODE_INNER) child<MAXV, STATS>(p, s.nodes, s.groups, G, dn, ch, x, pos, etr, e1, e2, c);
+                if (dn.flags & NODE_INNER) child<MAXV, STATS, true>(p, s.nodes, s.groups, G, dn, ch, x, pos, etr, e1, e2, c);
             }
         }
     }
+    close_chunk<MAXV>(p, c);
     flush<STATS>(p, s, c);
 }
 
@@ -568,6 +607,7 @@ __global__ void __launch_bounds__(kTB) long_kernel(const __grid_constant__ BPara
     c.tot = s.tot;
 #pragma unroll
     for (int i = 0; i < ST_N; i++) c.st[i] = 0;
+    c.em_next = c.em_end = 0;
     const int lane_id = threadIdx.x & 31;
     const uint32_t n_items = min(*(volatile uint32_t *)p.long_cnt, p.long_cap);
     const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -598,7 +638,7 @@ __global__ void __launch_bounds__(kTB) long_kernel(const __grid_constant__ BPara
                     if (STATS) c.st[ST_MATCHES] += __popc(mc);
                 }
                 if ((dn.flags & NODE_INNER) && hit)
-                    child<MAXV, STATS>(p, s.nodes, s.groups, G, dn, ch, x, pos, etr, e1, e2, c);
+                    child<MAXV, STATS, false>(p, s.nodes, s.groups, G, dn, ch, x, pos, etr, e1, e2, c);
             }
             if (STATS) {
                 const uint32_t we = __popc(__ballot_sync(kFull, w));

@@ -192,6 +192,17 @@ KernelKind kernel_kind() {
     }
     return (KernelKind)v;
 }
+// hybrid: a root is split breadth-first only if one of its windows has >= this many
+// entries (MAYURA_HEAVY_MIN; default 0 = split every root, the best setting on C1/C2 --
+// hub-dominated graphs; 8-16 is ~5-10 % faster on C3, see profiles/README.md)
+uint32_t heavy_min() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MAYURA_HEAVY_MIN");
+        v = e ? std::max(0, atoi(e)) : 0;
+    }
+    return (uint32_t)v;
+}
 // hybrid: breadth-first levels before the depth-first lane kernel (MAYURA_HYBRID_LEVELS)
 uint32_t hybrid_levels() {
     static int v = -1;
@@ -422,7 +433,7 @@ lane::LParams lane_params(const mayura_graph_s *g, const DeviceTable &dt, uint32
     q.n_frames = dt.max_edges > 2 ? dt.max_edges - 2 : 0;
     q.r0 = r0; q.n_roots = n_roots; q.lb = lb; q.counts = counts; q.stats = stats;
     q.dbg = dbg ? g->d_dbg : nullptr;
-    q.pm = nullptr; q.pm_cnt = nullptr; q.pm_seg_cap = 0; q.pm_words = 0;
+    q.pm = nullptr; q.pm_cnt = nullptr; q.pm_seg_cap = 0; q.pm_words = 0; q.heavy_min = 0;
     return q;
 }
 
@@ -442,6 +453,7 @@ bfs::BParams bfs_params(const mayura_graph_s *g, const DeviceTable &dt, uint32_t
     b.long_items = g->d_bfs_long; b.long_cap = g->bfs_long_cap;
     b.fallback = g->d_bfs_ctl + kCtlWords * bfs::kMaxLevels;
     b.inline_preleaf = inline_preleaf;
+    b.heavy_min = 0;  // set by mine() for the hybrid's single breadth-first level
     b.counts = counts; b.stats = stats;
     return b;
 }
@@ -462,6 +474,7 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         uint32_t *ctl = g->d_bfs_ctl;
         CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * (kCtlWords * bfs::kMaxLevels + 16), s), "cudaMemsetAsync(ctl)");
         bfs::BParams b = bfs_params(g, dt, r0, n_roots, counts, stats, kind == K_BFS ? 1u : 0u);
+        if (kind == K_HYBRID && levels == 1) b.heavy_min = heavy_min();
         uint32_t *bufs[2] = {g->d_bfs[0], g->d_bfs[1]};
         CK(launch_bfs(b, dt.max_vertices, levels, bufs, ctl, g->bfs_seg_cap, st, s, sms), "bfs pass launch");
         if (kind == K_BFS) return MAYURA_OK;
@@ -469,6 +482,7 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         q.pm_cnt = ctl + (levels - 1) * kCtlWords;
         q.pm_seg_cap = g->bfs_seg_cap;
         q.pm_words = words;
+        q.heavy_min = (levels == 1) ? heavy_min() : 0u;
     }
     CK(launch_lane(q, dt.max_vertices, st, dt.generic, s, sms), "comine_lane_kernel launch");
     return MAYURA_OK;

@@ -61,6 +61,9 @@ struct LParams {
     const uint32_t *pm;                 // null: root edges [r0, r0 + n_roots)
     const uint32_t *pm_cnt;             // kPmStripes counters
     uint32_t pm_seg_cap, pm_words;
+    uint32_t heavy_min;                 // hybrid: also mine the LIGHT roots of [r0, r0 + n_roots)
+                                        // (heavy ones were split by the breadth-first level, which
+                                        // also counted every root's completion); 0: no roots
     unsigned long long *counts;
     unsigned long long *stats;
 };
@@ -85,6 +88,25 @@ __host__ __device__ inline size_t smem_total(uint32_t nn, uint32_t ng, uint32_t 
 
 // m2g[k] == kNone for every motif vertex k that is not mapped (k >= nv), so the class
 // of a graph vertex is one compare per slot (vertex ids are < 2^31).
+// Hybrid split rule, applied identically by the breadth-first level (bfs.cuh) and this
+// kernel: a root is heavy if one of its root-node windows that starts from the root's own
+// successor pointers (START_P*/START_R*) has >= hmin entries (one probe load per window).
+template <int MAXV>
+__device__ __forceinline__ bool heavy_root(const LNode *nodes, const DGroup *groups, const LNode &root, const uint4 &P,
+                                           uint32_t h, const uint2 *out_ent, const uint2 *in_ent, uint32_t hmin) {
+    bool heavy = false;
+    for (uint32_t g = root.group_begin; g < root.group_end && !heavy; ++g) {
+        const DGroup G = groups[g];
+        if (G.start >= START_SEARCH) continue;
+        const uint32_t k = G.start < START_R0 ? G.start : G.start - START_R0;
+        const uint32_t start = k == 0 ? P.x : k == 1 ? P.y : k == 2 ? P.z : P.w;
+        const uint2 *ent = (G.kind == ANCHOR_OUT) ? out_ent : in_ent;
+        heavy = __ldg(&ent[start + hmin - 1].x) <= h;
+    }
+    (void)nodes;
+    return heavy;
+}
+
 template <int MAXV>
 __device__ __forceinline__ uint32_t classify(const uint32_t (&m)[MAXV], uint32_t x) {
     uint32_t c = CLS_NEW;
@@ -170,7 +192,9 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
 
     const LNode root = s_nodes[0];
     const bool root_inner = (root.flags & NODE_INNER) != 0;
-    const uint32_t n_items = p.pm ? s_pref[kPmStripes] : p.n_roots;
+    const uint32_t n_pm = p.pm ? s_pref[kPmStripes] : 0u;
+    const bool with_roots = !p.pm || p.heavy_min;
+    const uint32_t n_items = n_pm + (with_roots ? p.n_roots : 0u);
 
     // ------------------------------------------------------------ lane state
     bool active = false, scan = false, help = false, fresh = false;
@@ -251,8 +275,8 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
             const uint32_t take = min((uint32_t)__popc(need), cl);
             const uint32_t rank = __popc(need & lt_mask);
             const bool mine = ((need >> lane) & 1u) && rank < take;
-            if (mine && p.pm) {  // a partial match: its node's completion was counted when it was made
-                const uint32_t item = cb + rank;
+            const uint32_t item = cb + rank;
+            if (mine && item < n_pm) {  // a partial match: its node's completion was counted when it was made
                 int lo = 0, hi2 = kPmStripes - 1;
                 while (lo < hi2) {
                     const int mid = (lo + hi2 + 1) >> 1;
@@ -265,6 +289,8 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                 node = a.x & 0xffffu;
                 nv = a.x >> 16;
                 const uint32_t rt = a.y;
+                const bool hole = node == 0xFFFFu;  // unused slot of a reserved run (bfs::kHole)
+                if (hole) node = 0;
                 tr_prev = a.z;
                 h = a.w;
                 P = b4;
@@ -276,17 +302,19 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                     if (4 * q + 2 < MAXV) m2g[(4 * q + 2) % MAXV] = m4.z;
                     if (4 * q + 3 < MAXV) m2g[(4 * q + 3) % MAXV] = m4.w;
                 }
-                R = __ldg(p.eptr + rt);
-                const LNode dn = s_nodes[node];
-                g = dn.group_begin; g_end = dn.group_end;
-                lim = kNone; d = 0; scan = false; age = 0;
-                active = true;
+                if (!hole) {
+                    R = __ldg(p.eptr + rt);
+                    const LNode dn = s_nodes[node];
+                    g = dn.group_begin; g_end = dn.group_end;
+                    lim = kNone; d = 0; scan = false; age = 0;
+                    active = true;
+                }
             } else if (mine) {
-                const uint32_t r = p.r0 + cb + rank;
+                const uint32_t r = p.r0 + (item - n_pm);
                 const uint32_t rs = __ldg(p.src + r), rd = __ldg(p.dst + r);
                 if (rs != rd) {  // a self-loop never matches canonical 0->1 (reading R7)
-                    if (root.flags & NODE_COMPLETION) count_n(root.slot, tid, 1);
-                    if (STATS) {
+                    if (!p.pm && (root.flags & NODE_COMPLETION)) count_n(root.slot, tid, 1);
+                    if (STATS && !p.pm) {  // hybrid: the breadth-first level accounted for every root
                         st[ST_ROOTS]++;
                         st[ST_BYTES] += 16 + (root_inner ? 16 : 0);
                         st[ST_MATCHES] += (root.flags & NODE_COMPLETION) ? 1 : 0;
@@ -302,10 +330,12 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                         P = R;
                         node = 0; nv = 2; g = root.group_begin; g_end = root.group_end;
                         lim = kNone; d = 0; scan = false; age = 0;
-                        active = true;
-                        if (STATS) st[ST_NODES]++;
+                        // hybrid: a heavy root was split by the breadth-first level
+                        active = !(p.pm && heavy_root<MAXV>(s_nodes, s_groups, root, P, h, p.out_ent, p.in_ent,
+                                                            p.heavy_min));
+                        if (STATS && !p.pm) st[ST_NODES]++;
                     }
-                } else if (STATS) {
+                } else if (STATS && !p.pm) {
                     st[ST_BYTES] += 16;
                 }
             }
@@ -393,7 +423,8 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
             }
 
             // scan one entry of the current window
-            const DGroup G = s_groups[g];
+            const uint32_t gc = g;  // this entry's group (g may advance below when the window closes)
+            const DGroup G = s_groups[gc];
             uint32_t etr, e1, e2 = 0;
             const bool glob = GEN && G.kind == ANCHOR_GLOBAL;
             if (glob) {
@@ -404,10 +435,17 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                 } else {
                     e1 = 0;
                 }
-            } else {
-                const uint2 e = __ldg((G.kind == ANCHOR_OUT ? p.out_ent : p.in_ent) + pos);
+            }
+            // lists: the next entry is loaded with this one (independent load), so the window's
+            // terminator does not cost an iteration of its own
+            bool last = false;
+            if (!glob) {
+                const uint2 *lp = (G.kind == ANCHOR_OUT ? p.out_ent : p.in_ent) + pos;
+                const uint2 e = __ldg(lp);
+                const uint32_t nxt = __ldg(&lp[1].x);
                 etr = e.x;
                 e1 = e.y;
+                last = nxt > h;
             }
             if (STATS) st[ST_BATCHES]++;
             if (etr > h || pos >= lim) {  // window end
@@ -416,6 +454,10 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                 break;
             }
             ++pos;
+            if (last) {  // this entry closes the window: the next step starts the next group
+                ++g;
+                scan = false;
+            }
             if (etr <= tr_prev) break;  // before the window (lower-bound start)
             if (STATS) {
                 st[ST_ENTRIES]++;
@@ -428,8 +470,8 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
             else
                 cls = classify<MAXV>(m2g, e1);
             uint32_t hit = kNone;
-            if (G.child_end - G.child_begin <= 4 && g < kGwMax) {  // one SIMD byte compare
-                const uint32_t eq = __vcmpeq4(s_gw[g], cls * 0x01010101u);
+            if (G.child_end - G.child_begin <= 4 && gc < kGwMax) {  // one SIMD byte compare
+                const uint32_t eq = __vcmpeq4(s_gw[gc], cls * 0x01010101u);
                 hit = eq ? G.child_begin + ((__ffs(eq) - 1) >> 3) : kNone;
             } else {
                 for (uint32_t c = G.child_begin; c < G.child_end; ++c)
@@ -445,7 +487,8 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                 if (STATS) st[ST_MATCHES]++;
             }
             if (dn.flags & NODE_INNER) {
-                myfr[(d * kFrameWords + 0) * kLB] = node | (g << 16);
+                // the parent resumes at pos in its group (undo the early window close)
+                myfr[(d * kFrameWords + 0) * kLB] = node | (gc << 16);
                 myfr[(d * kFrameWords + 1) * kLB] = pos;
                 myfr[(d * kFrameWords + 2) * kLB] = tr_prev;
                 myfr[(d * kFrameWords + 3) * kLB] = lim;

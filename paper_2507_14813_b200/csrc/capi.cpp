@@ -119,9 +119,12 @@ extern "C" mayura_status mayura_partition_roots(mayura_graph g, int64_t delta, u
     clear_error();
     if (!g || !bounds_out || n_parts == 0) return fail(MAYURA_E_INVALID, "mayura_partition_roots: bad argument");
     if (delta < 0) return fail(MAYURA_E_INVALID, "mayura_partition_roots: delta < 0");
-    if (mayura_status s = ensure_host(g)) return s;
+    std::vector<int64_t> dev_t;  // a device-built graph: only the timestamps come back
+    if (!g->host_built) {
+        if (mayura_status s = copy_t_host(g, dev_t)) return s;
+    }
     const uint64_t E = g->E;
-    const std::vector<int64_t> &t = g->t;
+    const std::vector<int64_t> &t = g->host_built ? g->t : dev_t;
     std::vector<uint64_t> pref(E + 1, 0);
     uint64_t j = 0, k = 0;  // j: first index with t > t_r ; k: first index with t > t_r + delta
     for (uint64_t r = 0; r < E; r++) {

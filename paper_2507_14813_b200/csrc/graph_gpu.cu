@@ -302,6 +302,23 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     return MAYURA_OK;
 }
 
+// Timestamps of a device-built graph (edge-id order), for mayura_partition_roots.
+mayura_status copy_t_host(mayura_graph_s *g, std::vector<int64_t> &t) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(g->device);
+    try {
+        t.resize(g->E);
+    } catch (const std::bad_alloc &) {
+        cudaSetDevice(prev);
+        return fail(MAYURA_E_OOM, "copy_t_host: out of host memory");
+    }
+    const cudaError_t e = g->E ? cudaMemcpy(t.data(), g->d_t, 8 * g->E, cudaMemcpyDeviceToHost) : cudaSuccess;
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return fail(MAYURA_E_CUDA, std::string("copy_t_host: ") + cudaGetErrorString(e));
+    return MAYURA_OK;
+}
+
 // Host copies of a device-built graph, for the inspection / partitioning calls.
 mayura_status ensure_host(mayura_graph_s *g) {
     if (g->host_built || g->device < 0) return MAYURA_OK;

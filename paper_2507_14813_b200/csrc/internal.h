@@ -122,6 +122,7 @@ constexpr size_t kPadE = 32, kPadEnt = 64;
 mayura_status build_graph_device(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t E,
                                  uint32_t V, mayura_graph_s *g);
 mayura_status ensure_host(mayura_graph_s *g);
+mayura_status copy_t_host(mayura_graph_s *g, std::vector<int64_t> &t);
 // Library device memory comes from the device's stream-ordered pool with a retained release
 // threshold, so load / free / scratch-growth cycles reuse memory instead of paying
 // cudaMalloc / cudaFree (the e2e path builds and drops a graph per step).  dmalloc/dfree

@@ -244,6 +244,54 @@ def cascade_zipf(n_vertices: int, n_edges: int, span: int, alpha: float, p: floa
 
 
 # --------------------------------------------------------------------------
+# Planted AML patterns (C5; "fan-out/fan-in k = 3-6 within delta/2,
+# cycles 3-5 within delta, scatter-gather"; the pattern names follow the AML work the paper
+# cites)
+# --------------------------------------------------------------------------
+PLANT_KINDS = ("fan_out", "fan_in", "cycle", "scatter_gather")
+
+
+def plant_aml(n_patterns: int, n_vertices: int, span: int, delta: int, seed: int):
+    """n_patterns laundering-style patterns, kinds in rotation, each on fresh random vertices
+    (distinct within a pattern) with strictly increasing timestamps:
+      fan_out k (k = 3..6): s -> d_1..d_k inside delta/2;   fan_in k: s_1..s_k -> d inside delta/2;
+      cycle L (L = 3..5): v_0 -> v_1 -> ... -> v_{L-1} -> v_0 inside delta;
+      scatter_gather: s -> m_1, s -> m_2, then m_1 -> d, m_2 -> d inside delta.
+    Returns (src, dst, t, planted) with planted[kind][size] = number of instances."""
+    rng = np.random.default_rng(seed + 7_777_777)
+    out_s, out_d, out_t = [], [], []
+    planted = {k: {} for k in PLANT_KINDS}
+    for i in range(n_patterns):
+        kind = PLANT_KINDS[i % len(PLANT_KINDS)]
+        t0 = int(rng.integers(0, max(1, span - delta)))
+        if kind in ("fan_out", "fan_in"):
+            k = int(rng.integers(3, 7))
+            vs = rng.choice(n_vertices, k + 1, replace=False)
+            ts = t0 + np.sort(rng.choice(max(k, delta // 2), k, replace=False))
+            hub, others = int(vs[0]), vs[1:]
+            for v, tt in zip(others, ts):
+                out_s.append(hub if kind == "fan_out" else int(v))
+                out_d.append(int(v) if kind == "fan_out" else hub)
+                out_t.append(int(tt))
+            planted[kind][k] = planted[kind].get(k, 0) + 1
+        elif kind == "cycle":
+            L = int(rng.integers(3, 6))
+            vs = rng.choice(n_vertices, L, replace=False)
+            ts = t0 + np.sort(rng.choice(max(L, delta), L, replace=False))
+            for j in range(L):
+                out_s.append(int(vs[j])); out_d.append(int(vs[(j + 1) % L])); out_t.append(int(ts[j]))
+            planted[kind][L] = planted[kind].get(L, 0) + 1
+        else:
+            vs = rng.choice(n_vertices, 4, replace=False)
+            ts = t0 + np.sort(rng.choice(max(4, delta), 4, replace=False))
+            s_, m1, m2, d_ = (int(x) for x in vs)
+            for (a, b), tt in zip(((s_, m1), (s_, m2), (m1, d_), (m2, d_)), ts):
+                out_s.append(a); out_d.append(b); out_t.append(int(tt))
+            planted[kind][2] = planted[kind].get(2, 0) + 1
+    return (np.array(out_s, np.uint32), np.array(out_d, np.uint32), np.array(out_t, np.int64), planted)
+
+
+# --------------------------------------------------------------------------
 # Workload configs (BASELINE.json "configs", made concrete)
 # --------------------------------------------------------------------------
 DAY = 86400
@@ -265,11 +313,24 @@ class Config:
     burst_frac: float = 0.0
     burst_width: float = 600.0
     n_bursts: int = 0
+    planted: int = 0          # AML patterns planted on top of the background (C5)
 
     def graph(self):
-        return cascade_zipf(self.n_vertices, self.n_edges, self.span, self.alpha, self.p,
-                            self.tau, self.seed, self.burst_frac, self.burst_width,
-                            self.n_bursts)
+        if not self.planted:
+            return cascade_zipf(self.n_vertices, self.n_edges, self.span, self.alpha, self.p,
+                                self.tau, self.seed, self.burst_frac, self.burst_width,
+                                self.n_bursts)
+        return self.graph_planted()[:4]
+
+    def graph_planted(self):
+        """(src, dst, t, V, planted): background cascade-Zipf edges plus planted AML
+        patterns, n_edges in total, shuffled together."""
+        ps, pd, pt, planted = plant_aml(self.planted, self.n_vertices, self.span, self.delta, self.seed)
+        bs, bd, bt, V = cascade_zipf(self.n_vertices, self.n_edges - ps.size, self.span, self.alpha, self.p,
+                                     self.tau, self.seed, self.burst_frac, self.burst_width, self.n_bursts)
+        order = np.random.default_rng(self.seed + 1).permutation(self.n_edges)
+        return (np.concatenate([bs, ps])[order], np.concatenate([bd, pd])[order],
+                np.concatenate([bt, pt])[order], V, planted)
 
     def group(self) -> List[Motif]:
         return group(self.motifs)
@@ -291,7 +352,14 @@ CONFIGS: Dict[str, Config] = {
     "C4": Config("C4", "stackoverflow-temporal-shaped 2.6M nodes / 63.5M edges, delta=86400s, 16 motifs",
                  2_601_977, 63_497_050, int(7.6 * 365 * DAY), 86400, tuple(GROUP_C4), 2.5, 0.40,
                  600.0, 4),
+    # alpha calibrated as for C4 (at 2.0 the top vertex takes ~6 % of 500 M edges, ~1,000 per
+    # hour, and fan-out-4 at delta = 1 h explodes); 2.5 keeps hubs at ~25 edges per hour.
     "C5": Config("C5", "transaction-graph-shaped (AML) 10M nodes / 500M edges, delta=3600s, 8 motifs",
-                 10_000_000, 500_000_000, int(3.58 * 365 * DAY), 3600, tuple(GROUP_C5), 2.0, 0.40,
-                 120.0, 5),
+                 10_000_000, 500_000_000, int(3.58 * 365 * DAY), 3600, tuple(GROUP_C5), 2.5, 0.40,
+                 120.0, 5, planted=200_000),
+    # C5's recipe at 1/250 scale (same span density per vertex is NOT preserved: a test-sized
+    # instance the oracle finishes in full, for exact parity and the planted lower bounds)
+    "C5s": Config("C5s", "AML-shaped test instance 40k nodes / 2M edges, delta=3600s, 8 motifs",
+                  40_000, 2_000_000, 60 * DAY, 3600, tuple(GROUP_C5), 2.5, 0.40, 120.0, 55,
+                  planted=4_000),
 }

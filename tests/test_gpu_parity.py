@@ -269,3 +269,13 @@ def test_config_c4_sampled_parity(M, oracle_mod):
     cut = E // 2
     halves = [M.comine(g, tree, (0, cut)), M.comine(g, tree, (cut, E))]
     assert [x + y for x, y in zip(*halves)] == full
+
+
+def test_config_c5s_full_parity(M, oracle_mod):
+    """C5's AML recipe at test size (2 M edges with planted fan-in/fan-out/cycle/scatter-gather
+    patterns): exact parity in full, co-mined == independent."""
+    cfg = synth.CONFIGS["C5s"]
+    src, dst, t, V = cfg.graph()
+    exp = oracle_mod.backtrack(src, dst, t, V, cfg.group(), cfg.delta)
+    assert gpu_counts(M, src, dst, t, V, cfg.group(), cfg.delta) == exp
+    assert gpu_counts(M, src, dst, t, V, cfg.group(), cfg.delta, independent=True) == exp

@@ -189,3 +189,47 @@ def test_synthetic_config_c1_nontrivial(oracle_mod):
     assert src.size == cfg.n_edges
     counts = oracle_mod.backtrack(src, dst, t, V, cfg.group(), cfg.delta)
     assert all(c > 0 for c in counts), counts
+
+
+def _planted_lower_bounds(planted):
+    """Matches every planted AML pattern contributes by construction (P7): a fan-out (fan-in)
+    of k edges with increasing times holds C(k, 3) / C(k, 4) fan-out3/4 (fan-in3/4) tuples;
+    each planted L-cycle is one L-cycle match rooted at its first edge; each scatter-gather is
+    one (0->1, 0->2, 1->3, 2->3) match."""
+    from math import comb
+    lb = {"fan_out3": 0, "fan_out4": 0, "fan_in3": 0, "fan_in4": 0, "cycle3": 0, "cycle4": 0, "cycle5": 0,
+          "scatter_gather": planted["scatter_gather"].get(2, 0)}
+    for k, n in planted["fan_out"].items():
+        lb["fan_out3"] += n * comb(k, 3)
+        lb["fan_out4"] += n * comb(k, 4)
+    for k, n in planted["fan_in"].items():
+        lb["fan_in3"] += n * comb(k, 3)
+        lb["fan_in4"] += n * comb(k, 4)
+    for L, n in planted["cycle"].items():
+        lb["cycle%d" % L] += n
+    return lb
+
+
+def test_planted_aml_patterns(oracle_mod):
+    """The AML planting (C5 recipe) on its own: each pattern is found exactly as constructed
+    (no background edges), pinning both the generator and the oracle on these motifs."""
+    ps, pd, pt, planted = synth.plant_aml(60, 10_000, 10 * 86400, 3600, seed=3)
+    V = 10_000
+    motifs = synth.group(synth.GROUP_C5)
+    got = dict(zip(synth.GROUP_C5, oracle_mod.backtrack(ps, pd, pt, V, motifs, 3600)))
+    lb = _planted_lower_bounds(planted)
+    for name in synth.GROUP_C5:
+        assert got[name] >= lb[name], name
+    # isolated patterns on random vertices of a 10k-vertex graph rarely touch: equal counts
+    assert sum(got.values()) <= sum(lb.values()) + 5
+    assert lb["cycle3"] + lb["cycle4"] + lb["cycle5"] == sum(planted["cycle"].values())
+
+
+def test_c5s_planted_lower_bounds(oracle_mod):
+    """P7 on the C5 recipe (test-sized twin C5s): every planted pattern is counted."""
+    cfg = synth.CONFIGS["C5s"]
+    src, dst, t, V, planted = cfg.graph_planted()
+    assert src.size == cfg.n_edges
+    got = dict(zip(cfg.motifs, oracle_mod.backtrack(src, dst, t, V, cfg.group(), cfg.delta)))
+    for name, lb in _planted_lower_bounds(planted).items():
+        assert got[name] >= lb, name

@@ -111,38 +111,63 @@ extern "C" void mayura_free_mgtree(mayura_mgtree m) {
     delete m;
 }
 
-// Work-balanced contiguous split of the root ids: proxy work of root r
-// = 1 + |{e : t_r < t_e <= t_r + delta}|, computed with two pointers over the
-// time-sorted timestamps; cut points at equal shares of the prefix sum.
+// Work-balanced contiguous split of the root ids.  Proxy work of root r:
+//   p(r) = 1 + min(s_r, 65535)^2,  s_r = entries of the four adjacency lists at the root's
+//   endpoints (out(src), in(dst), out(dst), in(src)) with t_r < t <= t_r + delta
+// (the root's level-1 window sizes; squared because the search below a root grows with
+// products of window sizes).  Cut points at equal shares of the prefix sum:
+//   bounds[p] = first r with prefix(r) >= floor(total * p / P)  (non-decreasing).
+// Host graphs compute it here; device-built graphs on the GPU (graph_gpu.cu, same
+// integer arithmetic, same bounds).
+namespace mayura {
+uint64_t proxy_host(const mayura_graph_s *g, uint64_t r, uint32_t H) {
+    const uint32_t a = g->src[r], b = g->dst[r];
+    const uint32_t xs[4] = {a, b, b, a};
+    const std::vector<uint32_t> *offs[4] = {&g->out_off, &g->in_off, &g->out_off, &g->in_off};
+    const std::vector<uint32_t> *ents[4] = {&g->out_ent, &g->in_ent, &g->out_ent, &g->in_ent};
+    uint64_t s = 0;
+    for (int k = 0; k < 4; k++) {
+        uint32_t lo = g->eptr[4 * r + k], hi = (*offs[k])[xs[k] + 1] - 1;  // sentinel at hi
+        const uint32_t start = lo;
+        while (lo < hi) {  // first position with time rank > H
+            const uint32_t m = lo + (hi - lo) / 2;
+            if ((*ents[k])[2 * (size_t)m] > H) hi = m;
+            else lo = m + 1;
+        }
+        s += lo - start;
+    }
+    s = std::min<uint64_t>(s, 65535);
+    return 1 + s * s;
+}
+}  // namespace mayura
+
 extern "C" mayura_status mayura_partition_roots(mayura_graph g, int64_t delta, uint32_t n_parts,
                                                 uint64_t *bounds_out) {
     clear_error();
     if (!g || !bounds_out || n_parts == 0) return fail(MAYURA_E_INVALID, "mayura_partition_roots: bad argument");
     if (delta < 0) return fail(MAYURA_E_INVALID, "mayura_partition_roots: delta < 0");
-    std::vector<int64_t> dev_t;  // a device-built graph: only the timestamps come back
-    if (!g->host_built) {
-        if (mayura_status s = copy_t_host(g, dev_t)) return s;
-    }
     const uint64_t E = g->E;
-    const std::vector<int64_t> &t = g->host_built ? g->t : dev_t;
-    std::vector<uint64_t> pref(E + 1, 0);
-    uint64_t j = 0, k = 0;  // j: first index with t > t_r ; k: first index with t > t_r + delta
-    for (uint64_t r = 0; r < E; r++) {
-        const int64_t lim = (delta > INT64_MAX - t[r]) ? INT64_MAX : t[r] + delta;
-        if (j < r + 1) j = r + 1;
-        while (j < E && t[j] <= t[r]) j++;
-        if (k < j) k = j;
-        while (k < E && t[k] <= lim) k++;
-        pref[r + 1] = pref[r] + 1 + (k - j);
+    std::vector<uint64_t> cut(n_parts + 1, 0);  // raw first-index for each share
+    if (!g->host_built) {
+        if (mayura_status s = partition_device(g, delta, n_parts, cut.data())) return s;
+    } else {
+        const std::vector<int64_t> &t = g->t;
+        std::vector<uint64_t> pref(E + 1, 0);
+        uint64_t k = 0;  // first index with t > t_r + delta
+        for (uint64_t r = 0; r < E; r++) {
+            const int64_t lim = (delta > INT64_MAX - t[r]) ? INT64_MAX : t[r] + delta;
+            if (k < r + 1) k = r + 1;
+            while (k < E && t[k] <= lim) k++;
+            pref[r + 1] = pref[r] + proxy_host(g, r, (uint32_t)(k - 1));
+        }
+        const uint64_t total = pref[E];
+        for (uint32_t p = 1; p < n_parts; p++) {
+            const uint64_t target = (total / n_parts) * p + ((total % n_parts) * p) / n_parts;
+            cut[p] = (uint64_t)(std::lower_bound(pref.begin(), pref.end(), target) - pref.begin());
+        }
     }
-    const uint64_t total = pref[E];
     bounds_out[0] = 0;
-    for (uint32_t p = 1; p < n_parts; p++) {
-        const long double target = (long double)total * p / n_parts;
-        uint64_t b = (uint64_t)(std::lower_bound(pref.begin(), pref.end(), (uint64_t)target) - pref.begin());
-        b = std::min<uint64_t>(b, E);
-        bounds_out[p] = std::max(b, bounds_out[p - 1]);
-    }
+    for (uint32_t p = 1; p < n_parts; p++) bounds_out[p] = std::max(std::min<uint64_t>(cut[p], E), bounds_out[p - 1]);
     bounds_out[n_parts] = E;
     return MAYURA_OK;
 }

@@ -18,6 +18,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <mutex>
 #include <string>
@@ -135,6 +136,70 @@ __global__ void k_entry_ptr(const uint32_t *ids, const uint4 *eptr, uint32_t N, 
         const uint32_t e = ids[p];
         ptr[p] = e != 0xFFFFFFFFu ? eptr[e] : make_uint4(0, 0, 0, 0);
     }
+}
+
+// Partition proxy per root (capi.cpp): p(r) = 1 + min(s_r, 65535)^2 with s_r the level-1
+// window sizes at the root's endpoints; H = last edge id with t <= t_r + delta.
+__global__ void k_proxy(const int64_t *t, uint32_t E, int64_t delta, const uint32_t *src, const uint32_t *dst,
+                        const uint4 *eptr, const uint32_t *out_off, const uint2 *out_ent, const uint32_t *in_off,
+                        const uint2 *in_ent, unsigned long long *proxy) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < E; r += gridDim.x * blockDim.x) {
+        const int64_t x = t[r];
+        const int64_t lim = (delta > INT64_MAX - x) ? INT64_MAX : x + delta;
+        uint32_t a = r + 1, step = 1, b = E;  // first index with t > lim, galloping from r
+        while (a < E) {
+            const uint32_t probe = min(E - 1, a + step - 1);
+            if (t[probe] > lim) {
+                b = probe;
+                break;
+            }
+            a = probe + 1;
+            step <<= 1;
+        }
+        while (a < b) {
+            const uint32_t m = a + ((b - a) >> 1);
+            if (t[m] > lim) b = m;
+            else a = m + 1;
+        }
+        const uint32_t H = a - 1;
+        const uint4 P = eptr[r];
+        const uint32_t u = src[r], v = dst[r];
+        const uint32_t st[4] = {P.x, P.y, P.z, P.w}, xs[4] = {u, v, v, u};
+        unsigned long long s = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const uint32_t *off = (k == 0 || k == 2) ? out_off : in_off;
+            const uint2 *ent = (k == 0 || k == 2) ? out_ent : in_ent;
+            uint32_t lo = st[k], hi = off[xs[k] + 1] - 1;
+            while (lo < hi) {
+                const uint32_t m = lo + ((hi - lo) >> 1);
+                if (ent[m].x > H) hi = m;
+                else lo = m + 1;
+            }
+            s += lo - st[k];
+        }
+        s = s < 65535ull ? s : 65535ull;
+        proxy[r] = 1 + s * s;
+    }
+}
+
+// cut[p] = first r with inclusive_prefix[r] >= target_p, + 1  (index into the exclusive prefix)
+__global__ void k_cuts(const unsigned long long *inc, uint32_t E, uint32_t P, unsigned long long *cut) {
+    const uint32_t p = threadIdx.x + 1;
+    if (p >= P) return;
+    const unsigned long long total = E ? inc[E - 1] : 0ull;
+    const unsigned long long target = (total / P) * p + ((total % P) * p) / P;
+    if (target == 0) {
+        cut[p] = 0;
+        return;
+    }
+    uint32_t lo = 0, hi = E;
+    while (lo < hi) {
+        const uint32_t m = lo + ((hi - lo) >> 1);
+        if (inc[m] >= target) hi = m;
+        else lo = m + 1;
+    }
+    cut[p] = (unsigned long long)lo + 1;
 }
 
 struct Tmp {  // scratch freed at scope exit
@@ -299,6 +364,42 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     }
     GK(cudaGetLastError(), "graph build kernels");
     GK(cudaStreamSynchronize(s), "graph build");
+    return MAYURA_OK;
+}
+
+mayura_status partition_device(mayura_graph_s *g, int64_t delta, uint32_t n_parts, uint64_t *cut) {
+    if (n_parts > 1024) return fail(MAYURA_E_LIMIT, "mayura_partition_roots: more than 1024 parts");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(g->device);
+    struct Restore {
+        int d;
+        ~Restore() { cudaSetDevice(d); }
+    } restore{prev};
+    const uint32_t E = (uint32_t)g->E;
+    Tmp tmp;
+    unsigned long long *proxy, *inc, *dcut;
+    cudaStream_t s = nullptr;
+    GK(tmp.get(proxy, E), "cudaMalloc(proxy)");
+    GK(tmp.get(inc, E), "cudaMalloc(prefix)");
+    GK(tmp.get(dcut, n_parts + 1), "cudaMalloc(cuts)");
+    GK(cudaMemsetAsync(dcut, 0, 8 * (n_parts + 1), s), "memset");
+    if (E) {
+        k_proxy<<<blocks_for(E), kT, 0, s>>>(g->d_t, E, delta, g->d_src, g->d_dst, reinterpret_cast<const uint4 *>(g->d_eptr),
+                                             g->d_out_off, reinterpret_cast<const uint2 *>(g->d_out_ent), g->d_in_off,
+                                             reinterpret_cast<const uint2 *>(g->d_in_ent), proxy);
+        size_t need = 0;
+        GK(cub::DeviceScan::InclusiveSum(nullptr, need, proxy, inc, (int)E, s), "cub scan");
+        char *ct;
+        GK(tmp.get(ct, need), "cudaMalloc(tmp)");
+        GK(cub::DeviceScan::InclusiveSum(ct, need, proxy, inc, (int)E, s), "cub scan");
+        k_cuts<<<1, 1024, 0, s>>>(inc, E, n_parts, dcut);
+    }
+    GK(cudaGetLastError(), "partition kernels");
+    std::vector<unsigned long long> h(n_parts + 1);
+    GK(cudaMemcpyAsync(h.data(), dcut, 8 * (n_parts + 1), cudaMemcpyDeviceToHost, s), "D2H(cuts)");
+    GK(cudaStreamSynchronize(s), "partition");
+    for (uint32_t p = 0; p <= n_parts; p++) cut[p] = h[p];
     return MAYURA_OK;
 }
 

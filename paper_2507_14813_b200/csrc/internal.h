@@ -123,6 +123,9 @@ mayura_status build_graph_device(const uint32_t *src, const uint32_t *dst, const
                                  uint32_t V, mayura_graph_s *g);
 mayura_status ensure_host(mayura_graph_s *g);
 mayura_status copy_t_host(mayura_graph_s *g, std::vector<int64_t> &t);
+// device path of mayura_partition_roots: cut[p] (1 <= p < n_parts) = first root index whose
+// proxy prefix reaches floor(total * p / n_parts) (capi.cpp documents the proxy)
+mayura_status partition_device(mayura_graph_s *g, int64_t delta, uint32_t n_parts, uint64_t *cut);
 // Library device memory comes from the device's stream-ordered pool with a retained release
 // threshold, so load / free / scratch-growth cycles reuse memory instead of paying
 // cudaMalloc / cudaFree (the e2e path builds and drops a graph per step).  dmalloc/dfree

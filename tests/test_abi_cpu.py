@@ -148,15 +148,42 @@ def test_mgtree_errors(M):
     assert M.MGTree([[(2 * i, 2 * i + 1) for i in range(8)]], 1).info["max_vertices"] == 16
 
 
+def _partition_reference(ex, delta, parts):
+    """mayura_partition_roots' documented rule, re-derived in numpy from the exported arrays:
+    p(r) = 1 + min(s_r, 65535)^2, s_r = entries with t_r < t <= t_r + delta in out(src),
+    in(dst), out(dst), in(src); cuts at the first prefix reaching floor(total * p / P)."""
+    t, tr = ex["t"], ex["tr"].astype(np.int64)
+    E = t.size
+    H = np.searchsorted(t, t + delta, side="right") - 1          # last id with t <= t_r + delta
+    lists = [(ex["out_off"], ex["out_ent"], ex["src"]), (ex["in_off"], ex["in_ent"], ex["dst"]),
+             (ex["out_off"], ex["out_ent"], ex["dst"]), (ex["in_off"], ex["in_ent"], ex["src"])]
+    s = np.zeros(E, np.int64)
+    for k, (off, ent, who) in enumerate(lists):
+        keys = ent[0::2].astype(np.int64)
+        for r in range(E):
+            x = int(who[r])
+            lo, hi = int(ex["eptr"][r, k]), int(off[x + 1]) - 1
+            s[r] += int(np.searchsorted(keys[lo:hi], H[r], side="right"))
+    proxy = 1 + np.minimum(s, 65535) ** 2
+    pref = np.concatenate([[0], np.cumsum(proxy)])
+    total = int(pref[-1])
+    b = [0]
+    for q in range(1, parts):
+        target = (total // parts) * q + ((total % parts) * q) // parts
+        b.append(max(min(int(np.searchsorted(pref, target, side="left")), E), b[-1]))
+    return b + [E], proxy
+
+
 def test_partition_roots(M):
     src, dst, t, V = synth.CONFIGS["C1"].graph()
     g = M.Graph(src, dst, t, V, device=-1)
     for parts in (1, 2, 3, 8):
         b = g.partition(600, parts)
         assert b[0] == 0 and b[-1] == g.n_edges and all(x <= y for x, y in zip(b, b[1:]))
-    # balanced: proxy work per part within 2x of the mean on this graph
-    b = g.partition(600, 4)
-    ts = np.sort(t)
-    w = 1 + np.searchsorted(ts, ts + 600, side="right") - np.searchsorted(ts, ts, side="right")
-    per = [int(w[a:c].sum()) for a, c in zip(b, b[1:])]
-    assert max(per) < 1.2 * (sum(per) / 4)
+    ex = g.export()
+    for parts in (2, 4, 7):
+        ref, proxy = _partition_reference(ex, 600, parts)
+        b = g.partition(600, parts)
+        assert b == ref
+        per = [int(proxy[a:c].sum()) for a, c in zip(b, b[1:])]
+        assert max(per) <= sum(per) / parts + proxy.max()         # balanced up to one root

@@ -279,3 +279,15 @@ def test_config_c5s_full_parity(M, oracle_mod):
     exp = oracle_mod.backtrack(src, dst, t, V, cfg.group(), cfg.delta)
     assert gpu_counts(M, src, dst, t, V, cfg.group(), cfg.delta) == exp
     assert gpu_counts(M, src, dst, t, V, cfg.group(), cfg.delta, independent=True) == exp
+
+
+def test_partition_device_equals_host(M):
+    """mayura_partition_roots on a device-built graph (proxy + prefix sum + cuts on the GPU)
+    returns exactly the host-graph bounds."""
+    cases = [(synth.CONFIGS["C2"].graph(), 3600), (synth.CONFIGS["C1"].graph(), 600),
+             (synth.random_graph(5, 30, 3000, 200, self_loop_frac=0.05), 17), (([], [], [], 3), 5)]
+    for (src, dst, t, V), delta in cases:
+        gh = M.Graph(src, dst, t, V, device=-1)
+        gd = M.Graph(src, dst, t, V, device=0)
+        for parts in (1, 2, 3, 8, 64):
+            assert gd.partition(delta, parts) == gh.partition(delta, parts), (parts, delta)

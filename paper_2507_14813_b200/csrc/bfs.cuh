@@ -325,7 +325,8 @@ __device__ __forceinline__ void child(const BParams &p, const lane::LNode *nodes
                     short_ok = starts[i] + kLong > y.h + 1;
                 } else {
                     const uint2 *ent = (G2.kind == ANCHOR_OUT) ? p.out_ent : p.in_ent;
-                    short_ok = __ldg(&ent[starts[i] + kLong - 1].x) > y.h;
+                    const uint32_t *off = (G2.kind == ANCHOR_OUT) ? p.out_off : p.in_off;
+                    short_ok = !lane::window_has(ent, off, lane::m2g_get<MAXV>(y.m2g, G2.anchor), starts[i], kLong, y.h);
                 }
             }
         } else {
@@ -503,8 +504,8 @@ __global__ void __launch_bounds__(kTB) expand_kernel(const __grid_constant__ BPa
                 if (root.flags & NODE_INNER) c.st[ST_NODES]++;
             }
             if (!(root.flags & NODE_INNER)) continue;
-            if (p.heavy_min && !lane::heavy_root<MAXV>(s.nodes, s.groups, root, x.P, x.h, p.out_ent, p.in_ent,
-                                                        p.heavy_min))
+            if (p.heavy_min && !lane::heavy_root<MAXV>(s.nodes, s.groups, root, x.P, x.h, x.m2g[0], x.m2g[1],
+                                                        p.out_off, p.out_ent, p.in_off, p.in_ent, p.heavy_min))
                 continue;  // light root: the depth-first kernel takes it from the root range
         } else {
             load_rec<MAXV>(p, s.pref, item, x);
@@ -526,7 +527,8 @@ __global__ void __launch_bounds__(kTB) expand_kernel(const __grid_constant__ BPa
                 is_long = start + kLong <= x.h + 1;
             } else {
                 const uint2 *ent = (G.kind == ANCHOR_OUT) ? p.out_ent : p.in_ent;
-                is_long = __ldg(&ent[start + kLong - 1].x) <= x.h;
+                const uint32_t *off = (G.kind == ANCHOR_OUT) ? p.out_off : p.in_off;
+                is_long = lane::window_has(ent, off, lane::m2g_get<MAXV>(x.m2g, G.anchor), start, kLong, x.h);
             }
             if (is_long) {  // long window -> warp pass
                 const uint32_t li = atomicAdd(p.long_cnt, 1u);

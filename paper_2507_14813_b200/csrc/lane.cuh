@@ -88,20 +88,32 @@ __host__ __device__ inline size_t smem_total(uint32_t nn, uint32_t ng, uint32_t 
 
 // m2g[k] == kNone for every motif vertex k that is not mapped (k >= nv), so the class
 // of a graph vertex is one compare per slot (vertex ids are < 2^31).
+// Entries [start, start + k) of vertex x's list all lie inside the window (time rank <= h)?
+// The probe must stop at x's sentinel: the next vertex's list follows it, and its entries'
+// time ranks say nothing about this window.
+__device__ __forceinline__ bool window_has(const uint2 *ent, const uint32_t *off, uint32_t x, uint32_t start,
+                                           uint32_t k, uint32_t h) {
+    const uint32_t last = __ldg(off + x + 1) - 1;  // the sentinel's position
+    return start + k - 1 < last && __ldg(&ent[start + k - 1].x) <= h;
+}
+
 // Hybrid split rule, applied identically by the breadth-first level (bfs.cuh) and this
 // kernel: a root is heavy if one of its root-node windows that starts from the root's own
 // successor pointers (START_P*/START_R*) has >= hmin entries (one probe load per window).
 template <int MAXV>
 __device__ __forceinline__ bool heavy_root(const LNode *nodes, const DGroup *groups, const LNode &root, const uint4 &P,
-                                           uint32_t h, const uint2 *out_ent, const uint2 *in_ent, uint32_t hmin) {
+                                           uint32_t h, uint32_t rs, uint32_t rd, const uint32_t *out_off,
+                                           const uint2 *out_ent, const uint32_t *in_off, const uint2 *in_ent,
+                                           uint32_t hmin) {
     bool heavy = false;
     for (uint32_t g = root.group_begin; g < root.group_end && !heavy; ++g) {
         const DGroup G = groups[g];
         if (G.start >= START_SEARCH) continue;
         const uint32_t k = G.start < START_R0 ? G.start : G.start - START_R0;
         const uint32_t start = k == 0 ? P.x : k == 1 ? P.y : k == 2 ? P.z : P.w;
-        const uint2 *ent = (G.kind == ANCHOR_OUT) ? out_ent : in_ent;
-        heavy = __ldg(&ent[start + hmin - 1].x) <= h;
+        const uint32_t x = (k == 0 || k == 3) ? rs : rd;  // P/R order: out(src), in(dst), out(dst), in(src)
+        heavy = G.kind == ANCHOR_OUT ? window_has(out_ent, out_off, x, start, hmin, h)
+                                     : window_has(in_ent, in_off, x, start, hmin, h);
     }
     (void)nodes;
     return heavy;
@@ -331,8 +343,8 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                         node = 0; nv = 2; g = root.group_begin; g_end = root.group_end;
                         lim = kNone; d = 0; scan = false; age = 0;
                         // hybrid: a heavy root was split by the breadth-first level
-                        active = !(p.pm && heavy_root<MAXV>(s_nodes, s_groups, root, P, h, p.out_ent, p.in_ent,
-                                                            p.heavy_min));
+                        active = !(p.pm && heavy_root<MAXV>(s_nodes, s_groups, root, P, h, rs, rd, p.out_off,
+                                                            p.out_ent, p.in_off, p.in_ent, p.heavy_min));
                         if (STATS && !p.pm) st[ST_NODES]++;
                     }
                 } else if (STATS && !p.pm) {
@@ -413,7 +425,8 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                     // a long window of leaf children is scanned by the whole warp (below)
                     if (G.n_inner == 0 && G.kind != ANCHOR_GLOBAL) {
                         const uint2 *ent = (G.kind == ANCHOR_OUT) ? p.out_ent : p.in_ent;
-                        if (__ldg(&ent[pos + kHelpMin - 1].x) <= h) {
+                        const uint32_t *off = (G.kind == ANCHOR_OUT) ? p.out_off : p.in_off;
+                        if (window_has(ent, off, m2g_get<MAXV>(m2g, G.anchor), pos, kHelpMin, h)) {
                             help = true;
                             break;
                         }

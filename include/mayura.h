@@ -196,8 +196,13 @@ mayura_status mayura_partition_roots(mayura_graph g, int64_t delta, uint32_t n_p
 /* Thread-local message for the last failing call on this thread ("" if none). */
 const char *mayura_last_error(void);
 
-/* Library version string, e.g. "mayura-b200 0.1 sm_100a". */
+/* Library version string, e.g. "mayura-b200 0.2 sm_100a". */
 const char *mayura_version(void);
+
+/* Number of the library's own (hand-written) kernel launches enqueued so far in this
+ * process, all devices and handles (CUB's sort/scan launches inside the graph build are not
+ * included).  Monotonic; the difference around a call sequence is its launch count. */
+uint64_t mayura_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -20,7 +20,12 @@ using namespace mayura;
 
 extern "C" const char *mayura_last_error(void) { return g_last_error.c_str(); }
 
-extern "C" const char *mayura_version(void) { return "mayura-b200 0.1 sm_100a"; }
+extern "C" const char *mayura_version(void) { return "mayura-b200 0.2 sm_100a"; }
+
+namespace mayura {
+uint64_t launch_count();
+}
+extern "C" uint64_t mayura_launch_count(void) { return mayura::launch_count(); }
 
 extern "C" mayura_status mayura_graph_info(mayura_graph g, uint64_t *n_edges, uint32_t *n_vertices,
                                            uint64_t *device_bytes) {

@@ -155,6 +155,7 @@ cudaError_t launch_lane_t(const lane::LParams &p, size_t smem, cudaStream_t s, i
     const uint32_t need = (p.n_roots + lane::kLB - 1) / lane::kLB;
     if (need < grid) grid = need ? need : 1;
     kern<<<grid, lane::kLB, smem, s>>>(p);
+    count_launch();
     return cudaGetLastError();
 }
 
@@ -231,6 +232,7 @@ cudaError_t launch_bfs_pass(const bfs::BParams &p, bool long_pass, cudaStream_t 
         grid = std::max(1u, std::min(grid, need));
     }
     kern<<<grid, bfs::kTB, smem, s>>>(p);
+    count_launch();
     return cudaGetLastError();
 }
 
@@ -566,6 +568,7 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
         window_end_kernel<<<blocks, threads, 0, s>>>(g->d_t, (uint32_t)g->E, m->delta, (uint32_t)rb, n_roots,
                                                      g->d_hi, g->d_queue, n_lb, d_counts, k);
         CK(cudaGetLastError(), "window_end_kernel launch");
+        count_launch();
     }
     if (mid_event) CK(cudaEventRecord((cudaEvent_t)mid_event, s), "cudaEventRecord(mid_event)");
     const int sms = sm_count(g->device);

@@ -20,6 +20,7 @@
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <type_traits>
@@ -219,6 +220,10 @@ struct Tmp {  // scratch freed at scope exit
 
 }  // namespace
 
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
 int dmalloc(void **p, size_t bytes) {
     static std::mutex mu;
     static bool pooled[64] = {};
@@ -288,7 +293,10 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     GK(cudaMemcpyAsync(idst, hdst, 4ull * E, cudaMemcpyHostToDevice, s), "H2D(dst)");
     GK(cudaMemcpyAsync(it, ht, 8ull * E, cudaMemcpyHostToDevice, s), "H2D(t)");
     GK(cudaMemsetAsync(bad, 0, 16, s), "memset");
-    if (E) k_check_ids<<<blocks_for(E), kT, 0, s>>>(isrc, idst, E, V, bad);
+    if (E) {
+        k_check_ids<<<blocks_for(E), kT, 0, s>>>(isrc, idst, E, V, bad);
+        count_launch();
+    }
     // time range -> key bits
     int64_t *mm;
     GK(tmp.get(mm, 2), "cudaMalloc(tmp)");
@@ -316,16 +324,16 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     GK(tmp.get(key2, E), "cudaMalloc(tmp)");
     GK(tmp.get(val, E), "cudaMalloc(tmp)");
     if (E) {
-        k_iota_key<<<blocks_for(E), kT, 0, s>>>(it, tmin, key, val, E);
+        k_iota_key<<<blocks_for(E), kT, 0, s>>>(it, tmin, key, val, E); count_launch();
         const int tbits = std::max(1, bits_for((uint64_t)tmax - (uint64_t)tmin));
         size_t need = 0;
         GK(cub::DeviceRadixSort::SortPairs(nullptr, need, key, key2, val, g->d_perm, (int)E, 0, tbits, s), "cub sort");
         char *ct;
         GK(tmp.get(ct, need), "cudaMalloc(tmp)");
         GK(cub::DeviceRadixSort::SortPairs(ct, need, key, key2, val, g->d_perm, (int)E, 0, tbits, s), "cub sort");
-        k_gather<<<blocks_for(E), kT, 0, s>>>(g->d_perm, isrc, idst, it, g->d_src, g->d_dst, g->d_t, E);
+        k_gather<<<blocks_for(E), kT, 0, s>>>(g->d_perm, isrc, idst, it, g->d_src, g->d_dst, g->d_t, E); count_launch();
         // 2. time ranks
-        k_time_rank<<<blocks_for(E), kT, 0, s>>>(g->d_t, g->d_tr, E);
+        k_time_rank<<<blocks_for(E), kT, 0, s>>>(g->d_t, g->d_tr, E); count_launch();
     }
     // 3. out / in adjacency
     GK(tmp.get(skey, E), "cudaMalloc(tmp)");
@@ -340,27 +348,29 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
         uint2 *ent = reinterpret_cast<uint2 *>(dir == 0 ? g->d_out_ent : g->d_in_ent);
         GK(cudaMemsetAsync(ids[dir], 0xFF, 4 * (N + 1), s), "memset(ids)");
         if (E) {
-            k_iota<<<blocks_for(E), kT, 0, s>>>(val, E);
+            k_iota<<<blocks_for(E), kT, 0, s>>>(val, E); count_launch();
             size_t need = 0;
             GK(cub::DeviceRadixSort::SortPairs(nullptr, need, k_in, skey, val, val2, (int)E, 0, vbits, s), "cub sort");
             char *ct;
             GK(tmp.get(ct, need), "cudaMalloc(tmp)");
             GK(cub::DeviceRadixSort::SortPairs(ct, need, k_in, skey, val, val2, (int)E, 0, vbits, s), "cub sort");
-            k_scatter<<<blocks_for(E), kT, 0, s>>>(skey, val2, g->d_tr, nbr, E, ent, ids[dir]);
+            k_scatter<<<blocks_for(E), kT, 0, s>>>(skey, val2, g->d_tr, nbr, E, ent, ids[dir]); count_launch();
         }
-        k_offsets<<<blocks_for((uint64_t)V + 1), kT, 0, s>>>(skey, E, V, off);
+        k_offsets<<<blocks_for((uint64_t)V + 1), kT, 0, s>>>(skey, E, V, off); count_launch();
     }
     // 4. successor pointers, then each list entry's copy of them
-    if (E)
+    if (E) {
         k_succ<<<blocks_for(E), kT, 0, s>>>(g->d_src, g->d_dst, g->d_tr, g->d_out_off,
                                             reinterpret_cast<const uint2 *>(g->d_out_ent), g->d_in_off,
                                             reinterpret_cast<const uint2 *>(g->d_in_ent), E,
                                             reinterpret_cast<uint4 *>(g->d_eptr));
+        count_launch();
+    }
     if (N) {
         k_entry_ptr<<<blocks_for(N), kT, 0, s>>>(ids[0], reinterpret_cast<const uint4 *>(g->d_eptr),
-                                                 (uint32_t)N, reinterpret_cast<uint4 *>(g->d_out_ptr));
+                                                 (uint32_t)N, reinterpret_cast<uint4 *>(g->d_out_ptr)); count_launch();
         k_entry_ptr<<<blocks_for(N), kT, 0, s>>>(ids[1], reinterpret_cast<const uint4 *>(g->d_eptr),
-                                                 (uint32_t)N, reinterpret_cast<uint4 *>(g->d_in_ptr));
+                                                 (uint32_t)N, reinterpret_cast<uint4 *>(g->d_in_ptr)); count_launch();
     }
     GK(cudaGetLastError(), "graph build kernels");
     GK(cudaStreamSynchronize(s), "graph build");
@@ -387,13 +397,13 @@ mayura_status partition_device(mayura_graph_s *g, int64_t delta, uint32_t n_part
     if (E) {
         k_proxy<<<blocks_for(E), kT, 0, s>>>(g->d_t, E, delta, g->d_src, g->d_dst, reinterpret_cast<const uint4 *>(g->d_eptr),
                                              g->d_out_off, reinterpret_cast<const uint2 *>(g->d_out_ent), g->d_in_off,
-                                             reinterpret_cast<const uint2 *>(g->d_in_ent), proxy);
+                                             reinterpret_cast<const uint2 *>(g->d_in_ent), proxy); count_launch();
         size_t need = 0;
         GK(cub::DeviceScan::InclusiveSum(nullptr, need, proxy, inc, (int)E, s), "cub scan");
         char *ct;
         GK(tmp.get(ct, need), "cudaMalloc(tmp)");
         GK(cub::DeviceScan::InclusiveSum(ct, need, proxy, inc, (int)E, s), "cub scan");
-        k_cuts<<<1, 1024, 0, s>>>(inc, E, n_parts, dcut);
+        k_cuts<<<1, 1024, 0, s>>>(inc, E, n_parts, dcut); count_launch();
     }
     GK(cudaGetLastError(), "partition kernels");
     std::vector<unsigned long long> h(n_parts + 1);

@@ -130,7 +130,9 @@ mayura_status partition_device(mayura_graph_s *g, int64_t delta, uint32_t n_part
 // threshold, so load / free / scratch-growth cycles reuse memory instead of paying
 // cudaMalloc / cudaFree (the e2e path builds and drops a graph per step).  dmalloc/dfree
 // order on the legacy default stream; callers synchronise before first use on another stream.
-int dmalloc(void **p, size_t bytes);  // cudaError_t as int (keeps this header CUDA-free)
+int dmalloc(void **p, size_t bytes);
+// hand-written kernel launches enqueued by this library (mayura_launch_count)
+void count_launch(uint64_t n = 1);  // cudaError_t as int (keeps this header CUDA-free)
 void dfree(void *p);
 mayura_status build_graph_host(const uint32_t *src, const uint32_t *dst, const int64_t *t,
                                uint64_t E, uint32_t V, mayura_graph_s *g);

@@ -47,6 +47,7 @@ SIGNATURES = {
     "mayura_partition_roots": ([_P, _i64, _u32, _P], _int),
     "mayura_last_error": ([], ctypes.c_char_p),
     "mayura_version": ([], ctypes.c_char_p),
+    "mayura_launch_count": ([], _u64),
 }
 for _name, (_args, _res) in SIGNATURES.items():
     _f = getattr(_lib, _name)
@@ -85,6 +86,11 @@ def mayura_last_error() -> str:
 
 def mayura_version() -> str:
     return _lib.mayura_version().decode()
+
+
+def mayura_launch_count() -> int:
+    """The library's own kernel launches enqueued so far in this process."""
+    return int(_lib.mayura_launch_count())
 
 
 def mayura_load_graph(src, dst, t, n_vertices: int, device: int = 0) -> int:

@@ -193,16 +193,21 @@ KernelKind kernel_kind() {
     }
     return (KernelKind)v;
 }
-// hybrid: a root is split breadth-first only if one of its windows has >= this many
-// entries (MAYURA_HEAVY_MIN; default 0 = split every root, the best setting on C1/C2 --
-// hub-dominated graphs; 8-16 is ~5-10 % faster on C3, see profiles/README.md)
-uint32_t heavy_min() {
-    static int v = -1;
-    if (v < 0) {
+// hybrid: a root is split breadth-first only if one of its root-node windows has >= this
+// many entries.  Measured (profiles/README.md): graphs that fit in L2 gain from splitting
+// every root (frontier records are cheap there; C1/C2), DRAM-resident graphs from splitting
+// only roots with a window of >= 16 entries (C3 9.2 -> 6.2 ms, C4 110 -> 103 ms).
+// MAYURA_HEAVY_MIN overrides (0 = split every root).
+uint32_t heavy_min(const mayura_graph_s *g) {
+    static int v = -2;
+    if (v == -2) {
         const char *e = getenv("MAYURA_HEAVY_MIN");
-        v = e ? std::max(0, atoi(e)) : 0;
+        v = e ? std::max(0, atoi(e)) : -1;
     }
-    return (uint32_t)v;
+    if (v >= 0) return (uint32_t)v;
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
+    return g->graph_bytes <= (uint64_t)l2 ? 0u : 16u;
 }
 // hybrid: breadth-first levels before the depth-first lane kernel (MAYURA_HYBRID_LEVELS)
 uint32_t hybrid_levels() {
@@ -476,7 +481,7 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         uint32_t *ctl = g->d_bfs_ctl;
         CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * (kCtlWords * bfs::kMaxLevels + 16), s), "cudaMemsetAsync(ctl)");
         bfs::BParams b = bfs_params(g, dt, r0, n_roots, counts, stats, kind == K_BFS ? 1u : 0u);
-        if (kind == K_HYBRID && levels == 1) b.heavy_min = heavy_min();
+        if (kind == K_HYBRID && levels == 1) b.heavy_min = heavy_min(g);
         uint32_t *bufs[2] = {g->d_bfs[0], g->d_bfs[1]};
         CK(launch_bfs(b, dt.max_vertices, levels, bufs, ctl, g->bfs_seg_cap, st, s, sms), "bfs pass launch");
         if (kind == K_BFS) return MAYURA_OK;
@@ -484,7 +489,7 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         q.pm_cnt = ctl + (levels - 1) * kCtlWords;
         q.pm_seg_cap = g->bfs_seg_cap;
         q.pm_words = words;
-        q.heavy_min = (levels == 1) ? heavy_min() : 0u;
+        q.heavy_min = (levels == 1) ? heavy_min(g) : 0u;
     }
     CK(launch_lane(q, dt.max_vertices, st, dt.generic, s, sms), "comine_lane_kernel launch");
     return MAYURA_OK;

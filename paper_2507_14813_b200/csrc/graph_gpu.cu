@@ -280,6 +280,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     GK(alloc(g->d_in_ptr, 4 * (N + kPadE), 0), "cudaMalloc(in_ptr)");
     GK(alloc(g->d_perm, (size_t)E, -1), "cudaMalloc(perm)");
     g->device_bytes += bytes;
+    g->graph_bytes = bytes;
 
     Tmp tmp;
     uint32_t *isrc, *idst, *bad, *val, *val2, *skey, *ids[2];

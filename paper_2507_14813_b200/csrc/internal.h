@@ -97,6 +97,7 @@ struct mayura_graph_s {
     uint32_t bfs_words = 0;
     uint32_t bfs_seg_cap = 0, bfs_long_cap = 0;
     uint64_t device_bytes = 0;
+    uint64_t graph_bytes = 0;                            // the graph arrays alone (no scratch)
 };
 
 struct mayura_mgtree_s {

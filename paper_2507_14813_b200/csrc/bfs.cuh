@@ -63,6 +63,8 @@ struct BParams {
     uint32_t heavy_min;       // level 0 of the hybrid: a root is split breadth-first only if one of its
                               // windows has >= heavy_min entries; lighter roots are handed to the
                               // depth-first kernel whole, as a root record (0: split every root)
+    uint32_t *light;          // heavy_min > 0: the light roots, listed for the depth-first kernel (warp-
+    uint32_t *light_cnt;      //   aggregated appends; [0] = entries), so it needs no heavy test of its own
     unsigned long long *counts;
     unsigned long long *stats;
 };
@@ -488,29 +490,49 @@ __global__ void __launch_bounds__(kTB) expand_kernel(const __grid_constant__ BPa
     c.em_next = c.em_end = 0;
     const uint32_t n_items = LEVEL0 ? p.n_roots : s.pref[kStripes];
     const lane::LNode root = s.nodes[0];
-    for (uint32_t item = blockIdx.x * blockDim.x + threadIdx.x; item < n_items; item += gridDim.x * blockDim.x) {
+    const uint32_t lane_id = threadIdx.x & 31;
+    // warp-uniform trip count: each warp takes 32 consecutive items per iteration, so the
+    // light-root list can be appended with one ballot and one atomic per warp
+    for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n_items; base += gridDim.x * blockDim.x) {
+        const uint32_t item = base + lane_id;
         PM<MAXV> x;
+        bool go = item < n_items;  // this thread expands x breadth-first
         if (LEVEL0) {
+            bool light = false;
             const uint32_t r = p.r0 + item;
-            if (!load_root<MAXV>(p, r, x)) {
+            if (go && !load_root<MAXV>(p, r, x)) {
                 if (STATS) c.st[ST_BYTES] += 16;
-                continue;
+                go = false;
             }
-            if (root.flags & NODE_COMPLETION) count_add(c, root.slot, 1);
-            if (STATS) {
-                c.st[ST_ROOTS]++;
-                c.st[ST_BYTES] += 16 + ((root.flags & NODE_INNER) ? 16 : 0);
-                c.st[ST_MATCHES] += (root.flags & NODE_COMPLETION) ? 1 : 0;
-                if (root.flags & NODE_INNER) c.st[ST_NODES]++;
+            if (go) {
+                if (root.flags & NODE_COMPLETION) count_add(c, root.slot, 1);
+                if (STATS) {
+                    c.st[ST_ROOTS]++;
+                    c.st[ST_BYTES] += 16 + ((root.flags & NODE_INNER) ? 16 : 0);
+                    c.st[ST_MATCHES] += (root.flags & NODE_COMPLETION) ? 1 : 0;
+                    if (root.flags & NODE_INNER) c.st[ST_NODES]++;
+                }
+                if (!(root.flags & NODE_INNER)) go = false;
+                else if (p.heavy_min && !lane::heavy_root<MAXV>(s.nodes, s.groups, root, x.P, x.h, x.m2g[0], x.m2g[1],
+                                                                p.out_off, p.out_ent, p.in_off, p.in_ent, p.heavy_min)) {
+                    light = true;  // the depth-first kernel mines it whole
+                    go = false;
+                }
             }
-            if (!(root.flags & NODE_INNER)) continue;
-            if (p.heavy_min && !lane::heavy_root<MAXV>(s.nodes, s.groups, root, x.P, x.h, x.m2g[0], x.m2g[1],
-                                                        p.out_off, p.out_ent, p.in_off, p.in_ent, p.heavy_min))
-                continue;  // light root: the depth-first kernel takes it from the root range
-        } else {
+            if (p.light) {
+                const unsigned lm = __ballot_sync(kFull, light);
+                if (lm) {
+                    uint32_t b = 0;
+                    if (lane_id == 0) b = atomicAdd(p.light_cnt, (uint32_t)__popc(lm));
+                    b = __shfl_sync(kFull, b, 0);
+                    if (light) p.light[b + __popc(lm & ((1u << lane_id) - 1u))] = r;
+                }
+            }
+        } else if (go) {
             load_rec<MAXV>(p, s.pref, item, x);
-            if (x.node == kHole) continue;
+            go = x.node != kHole;
         }
+        if (!go) continue;
         const lane::LNode xn = s.nodes[x.node];
         for (uint32_t g = xn.group_begin; g < xn.group_end; ++g) {
             const DGroup G = s.groups[g];

@@ -162,9 +162,14 @@ cudaError_t launch_lane_t(const lane::LParams &p, size_t smem, cudaStream_t s, i
 constexpr size_t kLaneCntSmem = 48 * 1024;  // lane-private counters while they fit this budget
 
 template <int MAXV>
-cudaError_t launch_lane_v(const lane::LParams &p, bool stats, bool generic, cudaStream_t s, int sms) {
+cudaError_t launch_lane_v(lane::LParams p, bool stats, bool generic, cudaStream_t s, int sms) {
     const bool lanecnt = (size_t)p.n_slots * lane::kLB * 4 <= kLaneCntSmem;
     const size_t smem = lane::smem_total(p.n_nodes, p.n_groups, p.n_slots, p.n_frames, lanecnt, MAXV);
+    p.o_groups = (uint32_t)lane::off_groups(p.n_nodes);
+    p.o_tot = (uint32_t)lane::off_tot(p.n_nodes, p.n_groups);
+    p.o_cnt = (uint32_t)lane::off_cnt(p.n_nodes, p.n_groups, p.n_slots);
+    p.o_fr = (uint32_t)lane::off_frames(p.n_nodes, p.n_groups, p.n_slots, lanecnt);
+    p.o_stk = p.o_fr + (uint32_t)((p.n_frames ? p.n_frames : 1) * lane::kFrameWords * lane::kLB * 4);
     if (stats)  // the instrumented kernel is always the generic one
         return lanecnt ? launch_lane_t<MAXV, true, true, true>(p, smem, s, sms)
                        : launch_lane_t<MAXV, false, true, true>(p, smem, s, sms);
@@ -323,6 +328,8 @@ mayura_status ensure_bfs_buffers(mayura_graph_s *g, uint32_t words, int nbufs) {
         CK((cudaError_t)dmalloc((void **)&g->d_bfs_long, sizeof(uint32_t) * 3 * (size_t)g->bfs_long_cap),
            "cudaMalloc(long items)");
         g->device_bytes += sizeof(uint32_t) * 3 * (size_t)g->bfs_long_cap;
+        CK((cudaError_t)dmalloc((void **)&g->d_light, sizeof(uint32_t) * ((size_t)g->E + 32)), "cudaMalloc(light roots)");
+        g->device_bytes += sizeof(uint32_t) * ((size_t)g->E + 32);
     }
     return MAYURA_OK;
 }
@@ -441,6 +448,7 @@ lane::LParams lane_params(const mayura_graph_s *g, const DeviceTable &dt, uint32
     q.r0 = r0; q.n_roots = n_roots; q.lb = lb; q.counts = counts; q.stats = stats;
     q.dbg = dbg ? g->d_dbg : nullptr;
     q.pm = nullptr; q.pm_cnt = nullptr; q.pm_seg_cap = 0; q.pm_words = 0; q.heavy_min = 0;
+    q.light = nullptr; q.light_cnt = nullptr;
     return q;
 }
 
@@ -461,6 +469,8 @@ bfs::BParams bfs_params(const mayura_graph_s *g, const DeviceTable &dt, uint32_t
     b.fallback = g->d_bfs_ctl + kCtlWords * bfs::kMaxLevels;
     b.inline_preleaf = inline_preleaf;
     b.heavy_min = 0;  // set by mine() for the hybrid's single breadth-first level
+    b.light = nullptr;
+    b.light_cnt = g->d_bfs_ctl + kCtlWords * bfs::kMaxLevels + 1;
     b.counts = counts; b.stats = stats;
     return b;
 }
@@ -482,6 +492,7 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * (kCtlWords * bfs::kMaxLevels + 16), s), "cudaMemsetAsync(ctl)");
         bfs::BParams b = bfs_params(g, dt, r0, n_roots, counts, stats, kind == K_BFS ? 1u : 0u);
         if (kind == K_HYBRID && levels == 1) b.heavy_min = heavy_min(g);
+        if (b.heavy_min) b.light = g->d_light;  // light roots are listed for the depth-first kernel
         uint32_t *bufs[2] = {g->d_bfs[0], g->d_bfs[1]};
         CK(launch_bfs(b, dt.max_vertices, levels, bufs, ctl, g->bfs_seg_cap, st, s, sms), "bfs pass launch");
         if (kind == K_BFS) return MAYURA_OK;
@@ -490,6 +501,8 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         q.pm_seg_cap = g->bfs_seg_cap;
         q.pm_words = words;
         q.heavy_min = (levels == 1) ? heavy_min(g) : 0u;
+        q.light = b.light;
+        q.light_cnt = b.light_cnt;
     }
     CK(launch_lane(q, dt.max_vertices, st, dt.generic, s, sms), "comine_lane_kernel launch");
     return MAYURA_OK;
@@ -612,7 +625,7 @@ void free_device(mayura_graph_s *g) {
     DeviceGuard guard(g->device);
     void *ptrs[] = {g->d_src, g->d_dst, g->d_tr, g->d_hi, g->d_t, g->d_out_off, g->d_in_off, g->d_out_ent,
                     g->d_in_ent, g->d_eptr, g->d_out_ptr, g->d_in_ptr, g->d_perm, g->d_queue, g->d_counts,
-                    g->d_stats, g->d_dbg, g->d_bfs[0], g->d_bfs[1], g->d_bfs_ctl, g->d_bfs_long};
+                    g->d_stats, g->d_dbg, g->d_bfs[0], g->d_bfs[1], g->d_bfs_ctl, g->d_bfs_long, g->d_light};
     cudaDeviceSynchronize();  // no queued work may still use the memory returned to the pool
     for (void *p : ptrs) dfree(p);
     cudaStreamSynchronize(0);

@@ -64,8 +64,13 @@ struct LParams {
     uint32_t heavy_min;                 // hybrid: also mine the LIGHT roots of [r0, r0 + n_roots)
                                         // (heavy ones were split by the breadth-first level, which
                                         // also counted every root's completion); 0: no roots
+    const uint32_t *light;              // heavy_min > 0: the light roots the breadth-first level listed
+    const uint32_t *light_cnt;          //   ([0] = entries)
     unsigned long long *counts;
     unsigned long long *stats;
+    // dynamic shared-memory byte offsets (set by the launcher; kernel-constant operands instead
+    // of address arithmetic the compiler rematerialises under the 64-register cap)
+    uint32_t o_groups, o_tot, o_cnt, o_fr, o_stk;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -155,11 +160,11 @@ template <int MAXV, bool LANECNT, bool STATS, bool GEN>
 __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_constant__ LParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     LNode *s_nodes = reinterpret_cast<LNode *>(smem);
-    DGroup *s_groups = reinterpret_cast<DGroup *>(smem + off_groups(p.n_nodes));
-    unsigned long long *s_tot = reinterpret_cast<unsigned long long *>(smem + off_tot(p.n_nodes, p.n_groups));
-    uint32_t *s_cnt = reinterpret_cast<uint32_t *>(smem + off_cnt(p.n_nodes, p.n_groups, p.n_slots));
-    uint32_t *s_fr = reinterpret_cast<uint32_t *>(smem + off_frames(p.n_nodes, p.n_groups, p.n_slots, LANECNT));
-    uint32_t *s_stk = s_fr + (size_t)(p.n_frames ? p.n_frames : 1) * kFrameWords * kLB;
+    DGroup *s_groups = reinterpret_cast<DGroup *>(smem + p.o_groups);
+    unsigned long long *s_tot = reinterpret_cast<unsigned long long *>(smem + p.o_tot);
+    uint32_t *s_cnt = reinterpret_cast<uint32_t *>(smem + p.o_cnt);
+    uint32_t *s_fr = reinterpret_cast<uint32_t *>(smem + p.o_fr);
+    uint32_t *s_stk = reinterpret_cast<uint32_t *>(smem + p.o_stk);
     __shared__ uint32_t s_pref[kPmStripes + 1];
     __shared__ uint32_t s_gw[kGwMax];  // packed child wants (trees of <= kGwMax groups)
     for (uint32_t i = threadIdx.x; i < p.n_groups && i < kGwMax; i += kLB) s_gw[i] = p.gwant[i];
@@ -205,11 +210,11 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
     const LNode root = s_nodes[0];
     const bool root_inner = (root.flags & NODE_INNER) != 0;
     const uint32_t n_pm = p.pm ? s_pref[kPmStripes] : 0u;
-    const bool with_roots = !p.pm || p.heavy_min;
-    const uint32_t n_items = n_pm + (with_roots ? p.n_roots : 0u);
+    const uint32_t n_items = n_pm + (!p.pm ? p.n_roots : p.light ? *(volatile const uint32_t *)p.light_cnt : 0u);
 
     // ------------------------------------------------------------ lane state
     bool active = false, scan = false, help = false, fresh = false;
+    uint32_t chk = kNone;              // fresh leaf window: its anchor vertex, for the long-window probe
     uint32_t age = 0;                  // steps since this lane took its root / task
     uint32_t stop = 0;                 // warp-uniform: tasks on this warp's stack
     uint32_t m2g[MAXV];
@@ -321,12 +326,25 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                     lim = kNone; d = 0; scan = false; age = 0;
                     active = true;
                 }
+            } else if (mine && p.pm) {  // hybrid: a light root, mined whole (listed by the breadth-first level)
+                const uint32_t r = __ldg(p.light + (item - n_pm));
+#pragma unroll
+                for (int k = 2; k < MAXV; k++) m2g[k] = kNone;
+                m2g[0] = __ldg(p.src + r);
+                m2g[1] = __ldg(p.dst + r);
+                h = __ldg(p.hi + r);
+                tr_prev = __ldg(p.tr + r);
+                R = __ldg(p.eptr + r);
+                P = R;
+                node = 0; nv = 2; g = root.group_begin; g_end = root.group_end;
+                lim = kNone; d = 0; scan = false; age = 0;
+                active = true;
             } else if (mine) {
                 const uint32_t r = p.r0 + (item - n_pm);
                 const uint32_t rs = __ldg(p.src + r), rd = __ldg(p.dst + r);
                 if (rs != rd) {  // a self-loop never matches canonical 0->1 (reading R7)
-                    if (!p.pm && (root.flags & NODE_COMPLETION)) count_n(root.slot, tid, 1);
-                    if (STATS && !p.pm) {  // hybrid: the breadth-first level accounted for every root
+                    if (root.flags & NODE_COMPLETION) count_n(root.slot, tid, 1);
+                    if (STATS) {
                         st[ST_ROOTS]++;
                         st[ST_BYTES] += 16 + (root_inner ? 16 : 0);
                         st[ST_MATCHES] += (root.flags & NODE_COMPLETION) ? 1 : 0;
@@ -342,12 +360,10 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                         P = R;
                         node = 0; nv = 2; g = root.group_begin; g_end = root.group_end;
                         lim = kNone; d = 0; scan = false; age = 0;
-                        // hybrid: a heavy root was split by the breadth-first level
-                        active = !(p.pm && heavy_root<MAXV>(s_nodes, s_groups, root, P, h, rs, rd, p.out_off,
-                                                            p.out_ent, p.in_off, p.in_ent, p.heavy_min));
-                        if (STATS && !p.pm) st[ST_NODES]++;
+                        active = true;
+                        if (STATS) st[ST_NODES]++;
                     }
-                } else if (STATS && !p.pm) {
+                } else if (STATS) {
                     st[ST_BYTES] += 16;
                 }
             }
@@ -422,15 +438,9 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                         st[ST_WINDOWS]++;
                         st[ST_BYTES] += G.kind == ANCHOR_GLOBAL ? 12 : 8;  // the terminating entry
                     }
-                    // a long window of leaf children is scanned by the whole warp (below)
-                    if (G.n_inner == 0 && G.kind != ANCHOR_GLOBAL) {
-                        const uint2 *ent = (G.kind == ANCHOR_OUT) ? p.out_ent : p.in_ent;
-                        const uint32_t *off = (G.kind == ANCHOR_OUT) ? p.out_off : p.in_off;
-                        if (window_has(ent, off, m2g_get<MAXV>(m2g, G.anchor), pos, kHelpMin, h)) {
-                            help = true;
-                            break;
-                        }
-                    }
+                    // a long window of leaf children is scanned by the whole warp (below); the
+                    // probe is issued with the window's first entry (no extra round trip)
+                    if (G.n_inner == 0 && G.kind != ANCHOR_GLOBAL) chk = m2g_get<MAXV>(m2g, G.anchor);
                 }
                 scan = true;
             }
@@ -456,6 +466,15 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                 const uint2 *lp = (G.kind == ANCHOR_OUT ? p.out_ent : p.in_ent) + pos;
                 const uint2 e = __ldg(lp);
                 const uint32_t nxt = __ldg(&lp[1].x);
+                if (chk != kNone) {  // fresh leaf window: >= kHelpMin entries (within the anchor's list)?
+                    const uint32_t sent = __ldg((G.kind == ANCHOR_OUT ? p.out_off : p.in_off) + chk + 1) - 1;
+                    const uint32_t far = __ldg(&lp[kHelpMin - 1].x);
+                    chk = kNone;
+                    if (pos + kHelpMin - 1 < sent && far <= h) {
+                        help = true;
+                        break;
+                    }
+                }
                 etr = e.x;
                 e1 = e.y;
                 last = nxt > h;

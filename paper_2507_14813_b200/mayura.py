@@ -17,7 +17,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libmayura.so")
+LIB_PATH = os.environ.get("MAYURA_LIB_PATH") or os.path.join(_HERE, "lib", "libmayura.so")  # override: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError("libmayura.so not built (%s); run `python -m paper_2507_14813_b200.build` "

@@ -77,11 +77,12 @@ def main():
     if not kernels:
         raise SystemExit("kernel not found in report")
     name, data = kernels[0]
-    m = re.search(r"comine_kernel<\(int\)(\d+), \(int\)(\d+), \(bool\)(\d)>", name)
+    # mangled tag of this template instance: kernel<(int)6, (bool)1> -> kernelILi6ELb1E
+    m = re.search(r"(\w+)<([^<>]*)>\(", name)
+    tag = args.kernel
     if m:
-        tag = "comine_kernelILi%sELi%sELb%s" % m.groups()
-    else:
-        tag = args.kernel
+        args_ = re.findall(r"\((int|bool)\)(\d+)", m.group(2))
+        tag = m.group(1) + "I" + "".join(("Li%sE" if t == "int" else "Lb%sE") % v for t, v in args_)
     mp = line_map(args.so, lambda sec: tag in sec)
     base = min(int(r["Address"], 16) for r in data)
     agg = collections.defaultdict(lambda: [0.0, 0.0])

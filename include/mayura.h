@@ -184,6 +184,31 @@ mayura_status mayura_comine_ex(mayura_graph g, mayura_mgtree m, uint64_t root_be
 mayura_status mayura_comine_stats(mayura_graph g, mayura_mgtree m, uint64_t root_begin,
                                   uint64_t root_end, int independent, uint64_t *stats_out);
 
+/* ----------------------------------------------------------- enumeration ---
+ * mayura_enumerate -- list every match instead of counting it (the paper's second
+ * output: "a comprehensive list of all matching motifs (enumeration)", PAPER.md:130;
+ * query option "counted or enumerated"; Algo 1 l.201 / Algo 3 l.662
+ * add the match to an enumeration list).  Root edges [root_begin, root_end) as in
+ * mayura_comine; a match belongs to the range of its first edge (reading R16).
+ *   tuples_out     : uint32 words.  Motif q's matches occupy words
+ *                    [W_q, W_q + count_q * len_q), W_q = sum_{j<q} count_j * len_j
+ *                    (len_q = edges of motif q); each match is len_q consecutive
+ *                    words = the INPUT indices (positions in the src/dst/t arrays given
+ *                    to mayura_load_graph) of the matched edges in motif edge order
+ *                    (strictly increasing time).  The order of matches within a motif
+ *                    is unspecified.  Device memory on the graph's GPU if
+ *                    tuples_on_device == 1, else host memory.  NULL: size query only.
+ *   capacity_words : words available at tuples_out.
+ *   counts_out     : host, n_motifs uint64 (always filled, as mayura_comine).
+ *   words_needed   : host, may be NULL: sum_q count_q * len_q.
+ * Synchronises the stream.  Errors: E_INVALID (range, NULL handle / counts_out),
+ * E_STATE (host-only graph), E_LIMIT (capacity_words < words needed -- counts_out and
+ * words_needed are still filled; or > 96 distinct motifs in the group), E_CUDA. */
+mayura_status mayura_enumerate(mayura_graph g, mayura_mgtree m, uint64_t root_begin,
+                               uint64_t root_end, void *cuda_stream, uint32_t *tuples_out,
+                               uint64_t capacity_words, int tuples_on_device,
+                               uint64_t *counts_out, uint64_t *words_needed);
+
 /* ------------------------------------------------------------ multi-GPU ---
  * mayura_partition_roots -- split [0, E) into n_parts contiguous root ranges
  * (timestamp ranges) of balanced estimated work (proxy: 1 + number of edges in

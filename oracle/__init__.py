@@ -8,6 +8,8 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
   (§2.1), tuple enumeration; guarded to small graphs.
 * ``backtrack``   (O2) -- Algorithm 1 "Temporal Motif Mining",
   every motif mined independently, threaded over root edges.
+* ``enumerate_matches`` -- O2 in enumeration form (Algo 1 l.201): one row of
+  input edge indices per match, single-threaded.
 * ``python_bruteforce`` -- a second, independent brute force in pure Python
   (itertools), for tiny inputs only.
 
@@ -51,6 +53,8 @@ def _load():
         lib.oracle_bruteforce.restype = i32
         lib.oracle_backtrack.argtypes = [P, P, P, u64, u32, P, P, u32, i64, u64, u64, i32, P]
         lib.oracle_backtrack.restype = i32
+        lib.oracle_enumerate.argtypes = [P, P, P, u64, u32, P, u32, i64, u64, u64, P, u64, P]
+        lib.oracle_enumerate.restype = i32
         lib.oracle_sorted_order.argtypes = [P, u64, P]
         lib.oracle_sorted_order.restype = i32
         _lib = lib
@@ -102,6 +106,30 @@ def backtrack(src, dst, t, n_vertices: int, motifs: Sequence[Sequence[Tuple[int,
     if rc != 0:
         raise OracleError("oracle_backtrack failed rc=%d" % rc)
     return [int(x) for x in out]
+
+
+def enumerate_matches(src, dst, t, n_vertices: int, motif: Sequence[Tuple[int, int]], delta: int,
+                      root_range: Optional[Tuple[int, int]] = None) -> np.ndarray:
+    """O2 in enumeration form (Algo 1 l.201): a (count, m) array of input edge indices,
+    one row per match of `motif`, edges in motif order."""
+    lib = _load()
+    s, d, tt = _arr(src, np.uint32), _arr(dst, np.uint32), _arr(t, np.int64)
+    E = s.size
+    rb, re_ = root_range if root_range is not None else (0, E)
+    me = _arr([x for e in motif for x in e], np.uint32)
+    m = len(motif)
+    cnt = np.zeros(1, np.uint64)
+    rc = lib.oracle_enumerate(_ptr(s), _ptr(d), _ptr(tt), E, n_vertices, _ptr(me), m, int(delta), rb, re_,
+                              None, 0, _ptr(cnt))
+    if rc not in (0, -2):
+        raise OracleError("oracle_enumerate failed rc=%d" % rc)
+    n = int(cnt[0])
+    out = np.zeros(max(n * m, 1), np.uint32)
+    rc = lib.oracle_enumerate(_ptr(s), _ptr(d), _ptr(tt), E, n_vertices, _ptr(me), m, int(delta), rb, re_,
+                              _ptr(out), n, _ptr(cnt))
+    if rc != 0:
+        raise OracleError("oracle_enumerate failed rc=%d" % rc)
+    return out[:n * m].reshape(n, m)
 
 
 def sorted_order(t) -> np.ndarray:

@@ -11,7 +11,7 @@
  *   count(M, G, delta) = #{ (e_1..e_m) : t(e_1) < ... < t(e_m),  t(e_m) - t(e_1) <= delta,
  *                           exists injective phi: V_M -> V_G, phi(u_j)=src(e_j), phi(v_j)=dst(e_j) }
  *
- * Two implementations:
+ * Two implementations (+ O2's enumeration form, oracle_enumerate):
  *   O1  oracle_bruteforce  -- the definition written out: enumerate increasing
  *       tuples of edges in time order, test the window, then build phi edge by
  *       edge and test consistency + injectivity.  Guarded (small inputs only).
@@ -53,6 +53,7 @@ typedef struct {
     int64_t *t;
     uint64_t *out_off;   /* V+1 */
     uint64_t *out_eid;   /* E: out-edges of each vertex in increasing edge id (= time) order */
+    uint64_t *rank;      /* E: input rank (position in the caller's arrays) of each sorted edge */
 } og_graph;
 
 typedef struct { int64_t t; uint64_t rank; } og_key;
@@ -64,7 +65,7 @@ static int og_key_cmp(const void *a, const void *b) {
 }
 
 static void og_free(og_graph *g) {
-    free(g->src); free(g->dst); free(g->t); free(g->out_off); free(g->out_eid);
+    free(g->src); free(g->dst); free(g->t); free(g->out_off); free(g->out_eid); free(g->rank);
     memset(g, 0, sizeof(*g));
 }
 
@@ -80,12 +81,13 @@ static int og_build(og_graph *g, const uint32_t *src, const uint32_t *dst, const
     g->t = (int64_t *)malloc(8 * (E ? E : 1));
     g->out_off = (uint64_t *)calloc((size_t)V + 1, 8);
     g->out_eid = (uint64_t *)malloc(8 * (E ? E : 1));
-    if (!k || !g->src || !g->dst || !g->t || !g->out_off || !g->out_eid) { free(k); og_free(g); return -3; }
+    g->rank = (uint64_t *)malloc(8 * (E ? E : 1));
+    if (!k || !g->src || !g->dst || !g->t || !g->out_off || !g->out_eid || !g->rank) { free(k); og_free(g); return -3; }
     for (uint64_t i = 0; i < E; i++) { k[i].t = t[i]; k[i].rank = i; }
     qsort(k, E, sizeof(og_key), og_key_cmp);
     for (uint64_t i = 0; i < E; i++) {
         uint64_t r = k[i].rank;
-        g->src[i] = src[r]; g->dst[i] = dst[r]; g->t[i] = t[r];
+        g->src[i] = src[r]; g->dst[i] = dst[r]; g->t[i] = t[r]; g->rank[i] = r;
     }
     free(k);
     /* out adjacency: counting sort by source, edge ids visited in increasing order */
@@ -187,6 +189,8 @@ typedef struct {
     int32_t *g2m;      /* V entries, -1 = unmapped */
     uint32_t *incnt;   /* V entries */
     uint64_t count;
+    uint32_t *out;     /* enumeration list (Algo 1 l.201 "add to enumeration list"), or NULL */
+    uint64_t cap;      /* tuples that fit in out */
 } o2_ctx;
 
 /* RollOnEdge (Algo 1 lines 240-245) */
@@ -216,7 +220,12 @@ static int o2_struct_ok(const o2_ctx *c, uint32_t uM, uint32_t vM, uint32_t eu, 
 
 /* MatchEdge (Algo 1 lines 198-236) for motif edge e_M >= 1; e_M = 0 is the root loop. */
 static void o2_match_edge(o2_ctx *c, uint32_t eM) {
-    if (eM == c->m) { c->count++; return; }                 /* line 199-201 */
+    if (eM == c->m) {                                        /* line 199-201 */
+        if (c->out && c->count < c->cap)                     /* enumeration: input ranks of e_1..e_m */
+            for (uint32_t j = 0; j < c->m; j++) c->out[c->count * c->m + j] = (uint32_t)c->g->rank[c->e_stack[j]];
+        c->count++;
+        return;
+    }
     const og_graph *g = c->g;
     uint32_t uM = c->mu[eM], vM = c->mv[eM];
     int64_t uG = c->m2g[uM];                                 /* line 205 */
@@ -356,4 +365,43 @@ int oracle_sorted_order(const int64_t *t, uint64_t E, uint64_t *perm_out) {
     for (uint64_t i = 0; i < E; i++) perm_out[i] = k[i].rank;
     free(k);
     return 0;
+}
+
+/* Enumeration ("a comprehensive list of all matching motifs"; Algo 1
+ * l.201): O2 for ONE motif, single-threaded, writing each match as m words = the input
+ * ranks of its edges in motif edge order, in the order Algorithm 1 finds them.  At most
+ * cap_tuples tuples are written; *count_out = the number of matches (returns -2 if it
+ * exceeds cap_tuples). */
+int oracle_enumerate(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t E, uint32_t V,
+                     const uint32_t *motif_edges, uint32_t m, int64_t delta, uint64_t root_begin,
+                     uint64_t root_end, uint32_t *out, uint64_t cap_tuples, uint64_t *count_out) {
+    if (m == 0 || m > OR_MAX_EDGES || delta < 0 || root_begin > root_end || root_end > E) return -1;
+    uint32_t mu[OR_MAX_EDGES], mv[OR_MAX_EDGES];
+    for (uint32_t j = 0; j < m; j++) {
+        mu[j] = motif_edges[2 * j]; mv[j] = motif_edges[2 * j + 1];
+        if (mu[j] >= OR_MAX_LABEL || mv[j] >= OR_MAX_LABEL || mu[j] == mv[j]) return -1;
+    }
+    og_graph g;
+    int rc = og_build(&g, src, dst, t, E, V);
+    if (rc) return rc;
+    o2_ctx c;
+    memset(&c, 0, sizeof(c));
+    c.g = &g; c.mu = mu; c.mv = mv; c.m = m; c.delta = delta; c.out = out; c.cap = cap_tuples;
+    c.g2m = (int32_t *)malloc(4 * ((size_t)V + 1));
+    c.incnt = (uint32_t *)calloc((size_t)V + 1, 4);
+    if (!c.g2m || !c.incnt) { free(c.g2m); free(c.incnt); og_free(&g); return -3; }
+    for (uint32_t v = 0; v < V; v++) c.g2m[v] = -1;
+    for (int i = 0; i < OR_MAX_LABEL; i++) c.m2g[i] = -1;
+    for (uint64_t e = root_begin; e < root_end; e++) {       /* e_M = 0: every edge is a candidate */
+        uint32_t eu = g.src[e], ev = g.dst[e];
+        if (!o2_struct_ok(&c, mu[0], mv[0], eu, ev)) continue;
+        c.e_stack[0] = e; c.top = 1;
+        o2_roll_on(&c, mu[0], mv[0], eu, ev);
+        o2_match_edge(&c, 1);
+        c.top = 0;
+        o2_roll_back(&c, eu, ev);
+    }
+    *count_out = c.count;
+    free(c.g2m); free(c.incnt); og_free(&g);
+    return c.count > cap_tuples ? -2 : 0;
 }

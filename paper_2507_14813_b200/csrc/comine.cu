@@ -16,6 +16,8 @@
 // All arithmetic is integer (u32 ids and time ranks, i64 timestamps, u64 counts).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_scan.cuh>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -127,9 +129,9 @@ mayura_status cuda_fail(cudaError_t e, const char *what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, what); \
     } while (0)
 
-template <int MAXV, bool LANECNT, bool STATS, bool GEN>
-cudaError_t launch_lane_t(const lane::LParams &p, size_t smem, cudaStream_t s, int sms) {
-    auto kern = lane::comine_lane_kernel<MAXV, LANECNT, STATS, GEN>;
+template <int MAXV, bool LANECNT, bool STATS, bool GEN, bool ENUM = false>
+cudaError_t launch_lane_t(const lane::LParams &p, size_t smem, cudaStream_t s, int sms, uint32_t *grid_out = nullptr) {
+    auto kern = lane::comine_lane_kernel<MAXV, LANECNT, STATS, GEN, ENUM>;
     static std::mutex mu;
     static size_t cached_smem = 0;
     static int cached_dev = -1, cached_per_sm = 0;
@@ -154,6 +156,13 @@ cudaError_t launch_lane_t(const lane::LParams &p, size_t smem, cudaStream_t s, i
     uint32_t grid = (uint32_t)(sms * per_sm);
     const uint32_t need = (p.n_roots + lane::kLB - 1) / lane::kLB;
     if (need < grid) grid = need ? need : 1;
+    if (grid_out) {  // ENUM: the caller sizes the per-warp arrays from the grid first
+        if (*grid_out == 0) {
+            *grid_out = grid;
+            return cudaSuccess;
+        }
+        grid = *grid_out;
+    }
     kern<<<grid, lane::kLB, smem, s>>>(p);
     count_launch();
     return cudaGetLastError();
@@ -169,7 +178,9 @@ cudaError_t launch_lane_v(lane::LParams p, bool stats, bool generic, cudaStream_
     p.o_tot = (uint32_t)lane::off_tot(p.n_nodes, p.n_groups);
     p.o_cnt = (uint32_t)lane::off_cnt(p.n_nodes, p.n_groups, p.n_slots);
     p.o_fr = (uint32_t)lane::off_frames(p.n_nodes, p.n_groups, p.n_slots, lanecnt);
-    p.o_stk = p.o_fr + (uint32_t)((p.n_frames ? p.n_frames : 1) * lane::kFrameWords * lane::kLB * 4);
+    p.o_stk = (uint32_t)lane::off_stk(p.n_nodes, p.n_groups, p.n_slots, p.n_frames, lanecnt, false);
+    p.o_pre = (uint32_t)lane::off_pre(p.n_nodes, p.n_groups, p.n_slots, p.n_frames, lanecnt, MAXV, false);
+    p.o_enum = (uint32_t)lane::off_enum(p.n_nodes, p.n_groups, p.n_slots, p.n_frames, lanecnt, MAXV, false);
     if (stats)  // the instrumented kernel is always the generic one
         return lanecnt ? launch_lane_t<MAXV, true, true, true>(p, smem, s, sms)
                        : launch_lane_t<MAXV, false, true, true>(p, smem, s, sms);
@@ -178,6 +189,30 @@ cudaError_t launch_lane_v(lane::LParams p, bool stats, bool generic, cudaStream_
                        : launch_lane_t<MAXV, true, false, false>(p, smem, s, sms);
     return generic ? launch_lane_t<MAXV, false, false, true>(p, smem, s, sms)
                    : launch_lane_t<MAXV, false, false, false>(p, smem, s, sms);
+}
+
+// ENUM kernels (mayura_enumerate): lane counters always, no stats.  *grid == 0: only compute the
+// grid (returned in *grid); else launch on exactly that grid (both passes must agree).
+template <int MAXV>
+cudaError_t launch_enum_v(lane::LParams p, bool generic, cudaStream_t s, int sms, uint32_t *grid) {
+    const size_t smem = lane::smem_total(p.n_nodes, p.n_groups, p.n_slots, p.n_frames, true, MAXV, true);
+    p.o_groups = (uint32_t)lane::off_groups(p.n_nodes);
+    p.o_tot = (uint32_t)lane::off_tot(p.n_nodes, p.n_groups);
+    p.o_cnt = (uint32_t)lane::off_cnt(p.n_nodes, p.n_groups, p.n_slots);
+    p.o_fr = (uint32_t)lane::off_frames(p.n_nodes, p.n_groups, p.n_slots, true);
+    p.o_stk = (uint32_t)lane::off_stk(p.n_nodes, p.n_groups, p.n_slots, p.n_frames, true, true);
+    p.o_pre = (uint32_t)lane::off_pre(p.n_nodes, p.n_groups, p.n_slots, p.n_frames, true, MAXV, true);
+    p.o_enum = (uint32_t)lane::off_enum(p.n_nodes, p.n_groups, p.n_slots, p.n_frames, true, MAXV, true);
+    return generic ? launch_lane_t<MAXV, true, false, true, true>(p, smem, s, sms, grid)
+                   : launch_lane_t<MAXV, true, false, false, true>(p, smem, s, sms, grid);
+}
+
+cudaError_t launch_enum(const lane::LParams &p, uint32_t max_vertices, bool generic, cudaStream_t s, int sms,
+                        uint32_t *grid) {
+    if (max_vertices <= 4) return launch_enum_v<4>(p, generic, s, sms, grid);
+    if (max_vertices <= 6) return launch_enum_v<6>(p, generic, s, sms, grid);
+    if (max_vertices <= 8) return launch_enum_v<8>(p, generic, s, sms, grid);
+    return launch_enum_v<16>(p, generic, s, sms, grid);
 }
 
 cudaError_t launch_lane(const lane::LParams &p, uint32_t max_vertices, bool stats, bool generic, cudaStream_t s,
@@ -449,6 +484,8 @@ lane::LParams lane_params(const mayura_graph_s *g, const DeviceTable &dt, uint32
     q.dbg = dbg ? g->d_dbg : nullptr;
     q.pm = nullptr; q.pm_cnt = nullptr; q.pm_seg_cap = 0; q.pm_words = 0; q.heavy_min = 0;
     q.light = nullptr; q.light_cnt = nullptr;
+    q.enum_pass = 0; q.wcnt = nullptr; q.wpre = nullptr; q.slot_word = nullptr; q.slot_len = nullptr; q.out = nullptr;
+    q.perm = g->d_perm; q.out_rank = g->d_out_rank; q.in_rank = g->d_in_rank;
     return q;
 }
 
@@ -620,12 +657,147 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
     return MAYURA_OK;
 }
 
+// Enumeration (NEXT-3; "a comprehensive list of all matching motifs
+// (enumeration)", :412-413; Algo 1 l.201 / Algo 3 l.662 "add to the enumeration list").
+// Two passes of the depth-first lane kernel over the same static root-to-warp mapping:
+//   pass 1 counts per (completion slot, warp)   -> wcnt, and the per-motif counts
+//   exclusive scan of wcnt (CUB)                -> wpre: each warp's first tuple per slot
+//   pass 2 re-mines and writes every match      -> out, at exact positions (no holes)
+// then duplicate motifs (sharing a slot) get a device-to-device copy of their region.
+mayura_status run_enum(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t re, void *stream,
+                       uint32_t *out, uint64_t cap_words, int on_device, uint64_t *counts_out,
+                       uint64_t *words_needed) {
+    if (!g || !m) return fail(MAYURA_E_INVALID, "mayura_enumerate: NULL handle");
+    if (g->device < 0) return fail(MAYURA_E_STATE, "mayura_enumerate: graph is host-only (device = -1)");
+    if (rb > re || re > g->E) return fail(MAYURA_E_INVALID, "mayura_enumerate: bad root range");
+    if (!counts_out) return fail(MAYURA_E_INVALID, "mayura_enumerate: counts_out is NULL");
+    DeviceGuard guard(g->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<DeviceTable> tabs;
+    mayura_status st = ensure_tables(m, g->device, tabs);
+    if (st != MAYURA_OK) return st;
+    const DeviceTable &dt = tabs[0];
+    const uint32_t k = m->n_motifs, ns = dt.n_slots;
+    if ((size_t)ns * lane::kLB * 4 > kLaneCntSmem)
+        return fail(MAYURA_E_LIMIT, "mayura_enumerate: more than 96 distinct motifs in the group");
+    // slot of each motif (first-come order of the completion nodes) and the tuple length per slot
+    uint32_t n_slots_h = 0;
+    const std::vector<lane::LNode> ln = lane_nodes(m->group, n_slots_h);
+    std::vector<uint32_t> slot_of(k), slot_len(ns, 0), first_of(ns, kNone);
+    for (uint32_t q = 0; q < k; q++) {
+        slot_of[q] = ln[m->group.motif_node[q]].slot;
+        slot_len[slot_of[q]] = (uint32_t)m->canon[q].size();
+        if (first_of[slot_of[q]] == kNone) first_of[slot_of[q]] = q;
+    }
+    const uint32_t n_roots = (uint32_t)(re - rb);
+    const int sms = sm_count(g->device);
+    lane::LParams q = lane_params(g, dt, (uint32_t)rb, n_roots, nullptr, nullptr, nullptr, false);
+    uint32_t grid = 0;
+    CK(launch_enum(q, dt.max_vertices, dt.generic, s, sms, &grid), "enumeration grid");
+    const size_t nw = (size_t)grid * (lane::kLB / 32), nsw = (size_t)ns * nw;
+    size_t scan_bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const unsigned long long *)nullptr,
+                                     (unsigned long long *)nullptr, (int)std::max<size_t>(nsw, 1), s),
+       "cub scan size");
+    // scratch: counts k | wcnt nsw | wpre nsw | slot_word ns | slot_len ns | lb | scan temp
+    const size_t b_counts = 8 * (size_t)k, b_w = 8 * std::max<size_t>(nsw, 1), b_sw = 8 * (size_t)std::max(ns, 1u),
+                 b_sl = lane::align16(4 * (size_t)std::max(ns, 1u)), b_lb = 4 * LB_N * 4;
+    const size_t need_b = lane::align16(b_counts) + 2 * b_w + b_sw + b_sl + b_lb + scan_bytes + 256;
+    if (g->enum_bytes < need_b) {
+        if (g->d_enum) dfree(g->d_enum);
+        g->d_enum = nullptr;
+        g->enum_bytes = 0;
+        CK((cudaError_t)dmalloc((void **)&g->d_enum, need_b), "cudaMalloc(enumeration scratch)");
+        g->enum_bytes = need_b;
+    }
+    char *sc = reinterpret_cast<char *>(g->d_enum);
+    unsigned long long *d_counts = reinterpret_cast<unsigned long long *>(sc);
+    sc += lane::align16(b_counts);
+    unsigned long long *wcnt = reinterpret_cast<unsigned long long *>(sc);
+    sc += b_w;
+    unsigned long long *wpre = reinterpret_cast<unsigned long long *>(sc);
+    sc += b_w;
+    unsigned long long *d_sw = reinterpret_cast<unsigned long long *>(sc);
+    sc += b_sw;
+    uint32_t *d_sl = reinterpret_cast<uint32_t *>(sc);
+    sc += b_sl;
+    uint32_t *d_lb = reinterpret_cast<uint32_t *>(sc);
+    sc += b_lb;
+    void *d_scan = lane::align16((size_t)(sc - (char *)g->d_enum)) + (char *)g->d_enum;
+    CK(cudaStreamSynchronize(0), "cudaStreamSynchronize");
+    // pass 1: window ends (zeroes the counts) + per-warp counts
+    {
+        const int threads = 256;
+        uint32_t blocks = (n_roots + threads - 1) / threads;
+        blocks = std::max(blocks, (std::max<uint32_t>(LB_N, k) + threads - 1) / threads);
+        blocks = std::min<uint32_t>(std::max(blocks, 1u), 148u * 32u);
+        window_end_kernel<<<blocks, threads, 0, s>>>(g->d_t, (uint32_t)g->E, m->delta, (uint32_t)rb, n_roots,
+                                                     g->d_hi, d_lb, LB_N, d_counts, k);
+        CK(cudaGetLastError(), "window_end_kernel launch");
+        count_launch();
+    }
+    q.lb = d_lb;
+    q.counts = d_counts;
+    q.enum_pass = 1;
+    q.wcnt = wcnt;
+    if (n_roots > 0) CK(launch_enum(q, dt.max_vertices, dt.generic, s, sms, &grid), "enumeration pass 1");
+    std::vector<unsigned long long> cnt(k, 0);
+    CK(cudaMemcpyAsync(cnt.data(), d_counts, 8 * (size_t)k, cudaMemcpyDeviceToHost, s), "D2H(counts)");
+    CK(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    for (uint32_t i = 0; i < k; i++) counts_out[i] = cnt[i];
+    // regions in input motif order
+    std::vector<uint64_t> word(k + 1, 0);
+    for (uint32_t i = 0; i < k; i++) word[i + 1] = word[i] + cnt[i] * (uint64_t)m->canon[i].size();
+    if (words_needed) *words_needed = word[k];
+    if (!out) return MAYURA_OK;  // size query
+    if (cap_words < word[k]) return fail(MAYURA_E_LIMIT, "mayura_enumerate: capacity_words < words needed");
+    if (word[k] == 0) return MAYURA_OK;
+    std::vector<unsigned long long> sw(ns, 0);
+    for (uint32_t sl = 0; sl < ns; sl++) sw[sl] = first_of[sl] == kNone ? 0 : word[first_of[sl]];
+    CK(cudaMemcpyAsync(d_sw, sw.data(), 8 * (size_t)ns, cudaMemcpyHostToDevice, s), "H2D(slot words)");
+    CK(cudaMemcpyAsync(d_sl, slot_len.data(), 4 * (size_t)ns, cudaMemcpyHostToDevice, s), "H2D(slot lengths)");
+    CK(cub::DeviceScan::ExclusiveSum(d_scan, scan_bytes, wcnt, wpre, (int)nsw, s), "cub scan");
+    uint32_t *dout = out;
+    if (!on_device) {
+        CK((cudaError_t)dmalloc((void **)&dout, 4 * word[k]), "cudaMalloc(enumeration staging)");
+        CK(cudaStreamSynchronize(0), "cudaStreamSynchronize");
+    }
+    q.enum_pass = 2;
+    q.wpre = wpre;
+    q.slot_word = d_sw;
+    q.slot_len = d_sl;
+    q.out = dout;
+    mayura_status rs = MAYURA_OK;
+    cudaError_t e = launch_enum(q, dt.max_vertices, dt.generic, s, sms, &grid);
+    if (e != cudaSuccess) rs = cuda_fail(e, "enumeration pass 2");
+    for (uint32_t i = 0; i < k && rs == MAYURA_OK; i++) {  // duplicate motifs: copy the first one's tuples
+        const uint32_t q0 = first_of[slot_of[i]];
+        if (q0 != i && cnt[i]) {
+            e = cudaMemcpyAsync(dout + word[i], dout + word[q0], 4 * cnt[i] * m->canon[i].size(),
+                                cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) rs = cuda_fail(e, "D2D(duplicate motif)");
+        }
+    }
+    if (!on_device && rs == MAYURA_OK) {
+        e = cudaMemcpyAsync(out, dout, 4 * word[k], cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) rs = cuda_fail(e, "D2H(tuples)");
+    }
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess && rs == MAYURA_OK) rs = cuda_fail(e, "cudaStreamSynchronize");
+    if (!on_device) {
+        dfree(dout);
+        cudaStreamSynchronize(0);
+    }
+    return rs;
+}
+
 void free_device(mayura_graph_s *g) {
     if (g->device < 0) return;
     DeviceGuard guard(g->device);
     void *ptrs[] = {g->d_src, g->d_dst, g->d_tr, g->d_hi, g->d_t, g->d_out_off, g->d_in_off, g->d_out_ent,
                     g->d_in_ent, g->d_eptr, g->d_out_ptr, g->d_in_ptr, g->d_perm, g->d_queue, g->d_counts,
-                    g->d_stats, g->d_dbg, g->d_bfs[0], g->d_bfs[1], g->d_bfs_ctl, g->d_bfs_long, g->d_light};
+                    g->d_stats, g->d_dbg, g->d_bfs[0], g->d_bfs[1], g->d_bfs_ctl, g->d_bfs_long, g->d_light,
+                    g->d_out_rank, g->d_in_rank, g->d_enum};
     cudaDeviceSynchronize();  // no queued work may still use the memory returned to the pool
     for (void *p : ptrs) dfree(p);
     cudaStreamSynchronize(0);
@@ -717,4 +889,12 @@ extern "C" mayura_status mayura_comine_stats(mayura_graph g, mayura_mgtree m, ui
     if (!stats_out) return fail(MAYURA_E_INVALID, "mayura_comine_stats: stats_out is NULL");
     return run(g, m, root_begin, root_end, nullptr, nullptr, 0, independent ? 1 : 0,
                reinterpret_cast<unsigned long long *>(stats_out));
+}
+
+extern "C" mayura_status mayura_enumerate(mayura_graph g, mayura_mgtree m, uint64_t root_begin, uint64_t root_end,
+                                          void *cuda_stream, uint32_t *tuples_out, uint64_t capacity_words,
+                                          int tuples_on_device, uint64_t *counts_out, uint64_t *words_needed) {
+    clear_error();
+    return run_enum(g, m, root_begin, root_end, cuda_stream, tuples_out, capacity_words, tuples_on_device,
+                    counts_out, words_needed);
 }

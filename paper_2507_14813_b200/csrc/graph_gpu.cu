@@ -132,10 +132,12 @@ __global__ void k_succ(const uint32_t *src, const uint32_t *dst, const uint32_t 
     }
 }
 
-__global__ void k_entry_ptr(const uint32_t *ids, const uint4 *eptr, uint32_t N, uint4 *ptr) {
+__global__ void k_entry_ptr(const uint32_t *ids, const uint4 *eptr, const uint32_t *perm, uint32_t N, uint4 *ptr,
+                            uint32_t *rank) {
     for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
         const uint32_t e = ids[p];
         ptr[p] = e != 0xFFFFFFFFu ? eptr[e] : make_uint4(0, 0, 0, 0);
+        rank[p] = e != 0xFFFFFFFFu ? perm[e] : 0xFFFFFFFFu;
     }
 }
 
@@ -279,8 +281,12 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     GK(alloc(g->d_out_ptr, 4 * (N + kPadE), 0), "cudaMalloc(out_ptr)");
     GK(alloc(g->d_in_ptr, 4 * (N + kPadE), 0), "cudaMalloc(in_ptr)");
     GK(alloc(g->d_perm, (size_t)E, -1), "cudaMalloc(perm)");
-    g->device_bytes += bytes;
     g->graph_bytes = bytes;
+    // enumeration only (mayura_enumerate): input rank of the edge behind every list position
+    // (not read by the counting kernels, so not part of graph_bytes' residency estimate)
+    GK(alloc(g->d_out_rank, N + kPadE, 0xFF), "cudaMalloc(out_rank)");
+    GK(alloc(g->d_in_rank, N + kPadE, 0xFF), "cudaMalloc(in_rank)");
+    g->device_bytes += bytes;
 
     Tmp tmp;
     uint32_t *isrc, *idst, *bad, *val, *val2, *skey, *ids[2];
@@ -368,10 +374,12 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
         count_launch();
     }
     if (N) {
-        k_entry_ptr<<<blocks_for(N), kT, 0, s>>>(ids[0], reinterpret_cast<const uint4 *>(g->d_eptr),
-                                                 (uint32_t)N, reinterpret_cast<uint4 *>(g->d_out_ptr)); count_launch();
-        k_entry_ptr<<<blocks_for(N), kT, 0, s>>>(ids[1], reinterpret_cast<const uint4 *>(g->d_eptr),
-                                                 (uint32_t)N, reinterpret_cast<uint4 *>(g->d_in_ptr)); count_launch();
+        k_entry_ptr<<<blocks_for(N), kT, 0, s>>>(ids[0], reinterpret_cast<const uint4 *>(g->d_eptr), g->d_perm,
+                                                 (uint32_t)N, reinterpret_cast<uint4 *>(g->d_out_ptr), g->d_out_rank);
+        count_launch();
+        k_entry_ptr<<<blocks_for(N), kT, 0, s>>>(ids[1], reinterpret_cast<const uint4 *>(g->d_eptr), g->d_perm,
+                                                 (uint32_t)N, reinterpret_cast<uint4 *>(g->d_in_ptr), g->d_in_rank);
+        count_launch();
     }
     GK(cudaGetLastError(), "graph build kernels");
     GK(cudaStreamSynchronize(s), "graph build");

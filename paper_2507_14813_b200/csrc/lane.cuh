@@ -34,6 +34,11 @@ constexpr uint32_t kAgeMin = 64;        // steps on one search before its descen
 constexpr uint32_t kStackCap = 32;      // per-warp task stack (tasks)
 constexpr int kPmStripes = 64;          // segments of a partial-match source (bfs::kStripes)
 constexpr uint32_t kGwMax = 64;         // groups whose packed child wants are kept in shared memory
+constexpr int kPreMax = MAYURA_MAX_EDGES;  // ENUM: edges of a search's base prefix (root / task start)
+// ENUM frames carry one more word: the input rank of the edge matched when the frame was pushed
+__host__ __device__ constexpr int frame_words(bool en) { return en ? kFrameWords + 1 : kFrameWords; }
+// task-stack words per task: node|nv, tr_prev, h, P(4), R(4), m2g(MAXV) [+ ENUM: prefix length, prefix]
+__host__ __device__ constexpr int task_words(int maxv, bool en) { return 11 + maxv + (en ? 1 + kPreMax : 0); }
 
 struct __align__(4) LNode {  // 12 bytes
     uint8_t want, n_new, nv, flags;
@@ -70,7 +75,17 @@ struct LParams {
     unsigned long long *stats;
     // dynamic shared-memory byte offsets (set by the launcher; kernel-constant operands instead
     // of address arithmetic the compiler rematerialises under the 64-register cap)
-    uint32_t o_groups, o_tot, o_cnt, o_fr, o_stk;
+    uint32_t o_groups, o_tot, o_cnt, o_fr, o_stk, o_pre, o_enum;
+    // enumeration (ENUM kernels, mayura_enumerate): roots are mapped to warps
+    // statically (32-root chunk c -> warp c mod n_warps), so pass 1 (count per warp) and pass 2
+    // (write) see the same per-warp match sets and pass 2 writes at exact, prefix-summed positions
+    uint32_t enum_pass;                  // 1: per-warp counts into wcnt, 2: tuples into out
+    unsigned long long *wcnt;            // [slot * n_warps + warp]
+    const unsigned long long *wpre;      // exclusive prefix sum of wcnt
+    const unsigned long long *slot_word; // first word of a slot's tuple region in out
+    const uint32_t *slot_len;            // edges per tuple of a slot
+    uint32_t *out;                       // tuples: input ranks of the matched edges, in motif edge order
+    const uint32_t *perm, *out_rank, *in_rank;  // input rank of an edge id / of a list position's edge
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -85,10 +100,23 @@ __host__ __device__ inline size_t off_cnt(uint32_t nn, uint32_t ng, uint32_t ns)
 __host__ __device__ inline size_t off_frames(uint32_t nn, uint32_t ng, uint32_t ns, bool lanecnt) {
     return off_cnt(nn, ng, ns) + (lanecnt ? (size_t)ns * kLB * 4 : 0);
 }
+__host__ __device__ inline size_t off_stk(uint32_t nn, uint32_t ng, uint32_t ns, uint32_t nf, bool lanecnt, bool en) {
+    return off_frames(nn, ng, ns, lanecnt) + (size_t)(nf ? nf : 1) * frame_words(en) * kLB * 4;
+}
+__host__ __device__ inline size_t off_pre(uint32_t nn, uint32_t ng, uint32_t ns, uint32_t nf, bool lanecnt, int maxv,
+                                          bool en) {
+    return off_stk(nn, ng, ns, nf, lanecnt, en) + (size_t)(kLB / 32) * task_words(maxv, en) * kStackCap * 4;
+}
+// ENUM: per lane kPreMax prefix words; per (warp, slot) a u32 cursor and a u64 base; per slot
+// its u64 region start and u32 tuple length
+__host__ __device__ inline size_t off_enum(uint32_t nn, uint32_t ng, uint32_t ns, uint32_t nf, bool lanecnt, int maxv,
+                                           bool en) {
+    return align16(off_pre(nn, ng, ns, nf, lanecnt, maxv, en) + (en ? (size_t)kPreMax * kLB * 4 : 0));
+}
 __host__ __device__ inline size_t smem_total(uint32_t nn, uint32_t ng, uint32_t ns, uint32_t nf, bool lanecnt,
-                                             int maxv) {
-    return off_frames(nn, ng, ns, lanecnt) + (size_t)(nf ? nf : 1) * kFrameWords * kLB * 4 +
-           (size_t)(kLB / 32) * (11 + maxv) * kStackCap * 4;
+                                             int maxv, bool en = false) {
+    return off_enum(nn, ng, ns, nf, lanecnt, maxv, en) +
+           (en ? (size_t)(kLB / 32) * ns * 12 + (size_t)ns * 12 + 16 : 0);
 }
 
 // m2g[k] == kNone for every motif vertex k that is not mapped (k >= nv), so the class
@@ -156,8 +184,10 @@ __device__ __forceinline__ uint32_t pick4(const uint4 &v, uint32_t k) {
 
 // GEN: the tree has anchor groups that need a search (START_SEARCH) or scan the edge array
 // (GLOBAL); trees without them compile those paths out.
-template <int MAXV, bool LANECNT, bool STATS, bool GEN>
+template <int MAXV, bool LANECNT, bool STATS, bool GEN, bool ENUM = false>
 __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_constant__ LParams p) {
+    constexpr int FW = frame_words(ENUM);
+    constexpr int TW = task_words(MAXV, ENUM);
     extern __shared__ __align__(16) unsigned char smem[];
     LNode *s_nodes = reinterpret_cast<LNode *>(smem);
     DGroup *s_groups = reinterpret_cast<DGroup *>(smem + p.o_groups);
@@ -183,10 +213,31 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
     for (uint32_t i = tid; i < p.n_slots; i += kLB) s_tot[i] = 0;
     if (LANECNT)
         for (uint32_t i = 0; i < p.n_slots; i++) s_cnt[i * kLB + tid] = 0;
+    // ENUM: s_pre = per-lane base prefix; s_ecur/s_ebase = per (warp, slot) cursor / base (pass 1:
+    // u64 overflow of the lane counters); s_eword/s_elen = per-slot region start / tuple length
+    uint32_t *s_pre = reinterpret_cast<uint32_t *>(smem + p.o_pre);
+    unsigned long long *s_ebase = reinterpret_cast<unsigned long long *>(smem + p.o_enum);
+    unsigned long long *s_eword = s_ebase + (kLB / 32) * p.n_slots;
+    uint32_t *s_ecur = reinterpret_cast<uint32_t *>(s_eword + p.n_slots);
+    uint32_t *s_elen = s_ecur + (kLB / 32) * p.n_slots;
+    const uint32_t gwarp = blockIdx.x * (kLB / 32) + (threadIdx.x >> 5), n_warps = gridDim.x * (kLB / 32);
+    if (ENUM) {
+        for (uint32_t i = tid; i < (kLB / 32) * p.n_slots; i += kLB) {
+            const uint32_t w = i / p.n_slots, sl = i % p.n_slots;
+            const uint32_t gw = blockIdx.x * (kLB / 32) + w;
+            s_ecur[i] = 0;
+            s_ebase[i] = p.enum_pass == 2 ? p.wpre[(size_t)sl * n_warps + gw] - p.wpre[(size_t)sl * n_warps] : 0ull;
+        }
+        if (p.enum_pass == 2)
+            for (uint32_t i = tid; i < p.n_slots; i += kLB) {
+                s_eword[i] = p.slot_word[i];
+                s_elen[i] = p.slot_len[i];
+            }
+    }
     __syncthreads();
 
-    uint32_t *myfr = s_fr + tid;    // frame d, word f at myfr[(d * kFrameWords + f) * kLB]
-    uint32_t *wstk = s_stk + (size_t)(tid >> 5) * (11 + MAXV) * kStackCap;  // word q of slot i: [q * kStackCap + i]
+    uint32_t *myfr = s_fr + tid;    // frame d, word f at myfr[(d * FW + f) * kLB]
+    uint32_t *wstk = s_stk + (size_t)(tid >> 5) * TW * kStackCap;  // word q of slot i: [q * kStackCap + i]
     const uint32_t wbase = (uint32_t)tid & ~31u;
     // add n matches to lane `ln`'s counter of `slot` (ln = this lane, or a parked lane of
     // this warp whose window the warp scans for it)
@@ -196,6 +247,7 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
             uint32_t v = *c + n;
             if (v >= 0x80000000u) {
                 atomicAdd(&s_tot[slot], (unsigned long long)v);
+                if (ENUM) atomicAdd(&s_ebase[(ln >> 5) * p.n_slots + slot], (unsigned long long)v);
                 v = 0;
             }
             *c = v;
@@ -203,6 +255,19 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
             atomicAdd(&s_tot[slot], (unsigned long long)n);
         }
     };
+    // ENUM pass 2: write one tuple of `slot` for lane ln's search: its base prefix (bo words),
+    // the ranks in its frames 0..dd-1, then `last` (the matched edge; kNone: none)
+    auto emit = [&](uint32_t slot, uint32_t ln, uint32_t bo, uint32_t dd, uint32_t last) {
+        const uint32_t wi = (ln >> 5) * p.n_slots + slot;
+        const uint32_t idx = atomicAdd(&s_ecur[wi], 1u);
+        uint32_t *o = p.out + s_eword[slot] + (s_ebase[wi] + idx) * s_elen[slot];
+        for (uint32_t i = 0; i < bo; i++) *o++ = s_pre[i * kLB + ln];
+        for (uint32_t i = 0; i < dd; i++) *o++ = s_fr[(i * FW + kFrameWords) * kLB + ln];
+        if (last != kNone) *o = last;
+    };
+    const bool wr = ENUM && p.enum_pass == 2;
+    uint32_t bpre = 0;                 // ENUM: words of this lane's base prefix in s_pre
+    uint32_t wk = 0;                   // ENUM: chunks this warp has taken (static mapping)
     unsigned long long st[ST_N];
 #pragma unroll
     for (int i = 0; i < ST_N; i++) st[i] = 0;
@@ -258,6 +323,10 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                                    wstk[10 * kStackCap + slot]);
 #pragma unroll
                     for (int q = 0; q < MAXV; q++) m2g[q] = wstk[(11 + q) * kStackCap + slot];
+                    if (wr) {
+                        bpre = wstk[(11 + MAXV) * kStackCap + slot];
+                        for (uint32_t i = 0; i < bpre; i++) s_pre[i * kLB + tid] = wstk[(12 + MAXV + i) * kStackCap + slot];
+                    }
                     const LNode dn = s_nodes[node];
                     g = dn.group_begin;
                     g_end = dn.group_end;
@@ -274,14 +343,21 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
         while (need && roots_left) {
             if (cl == 0) {
                 uint32_t b = 0, sz = 0;
-                if (lane == 0) {
-                    const uint32_t cur = *(volatile uint32_t *)(p.lb + LB_ROOT);
-                    const uint32_t rem = cur < n_items ? n_items - cur : 0u;
-                    sz = max(32u, min(256u, rem / (4u * gridDim.x * (kLB / 32))));
-                    b = atomicAdd(p.lb + LB_ROOT, sz);
+                if (ENUM) {  // static: chunk gwarp + wk * n_warps (identical in both passes)
+                    b = (gwarp + wk * n_warps) * 32u;
+                    if ((b >> 5) != gwarp + wk * n_warps) b = n_items;  // overflow: no more chunks
+                    sz = 32;
+                    wk++;
+                } else {
+                    if (lane == 0) {
+                        const uint32_t cur = *(volatile uint32_t *)(p.lb + LB_ROOT);
+                        const uint32_t rem = cur < n_items ? n_items - cur : 0u;
+                        sz = max(32u, min(256u, rem / (4u * gridDim.x * (kLB / 32))));
+                        b = atomicAdd(p.lb + LB_ROOT, sz);
+                    }
+                    b = __shfl_sync(kFull, b, 0);
+                    sz = __shfl_sync(kFull, sz, 0);
                 }
-                b = __shfl_sync(kFull, b, 0);
-                sz = __shfl_sync(kFull, sz, 0);
                 if (b >= n_items) {
                     roots_left = false;
                     break;
@@ -343,7 +419,16 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                 const uint32_t r = p.r0 + (item - n_pm);
                 const uint32_t rs = __ldg(p.src + r), rd = __ldg(p.dst + r);
                 if (rs != rd) {  // a self-loop never matches canonical 0->1 (reading R7)
-                    if (root.flags & NODE_COMPLETION) count_n(root.slot, tid, 1);
+                    uint32_t rk = 0;
+                    if (wr) {
+                        rk = __ldg(p.perm + r);
+                        s_pre[tid] = rk;
+                        bpre = 1;
+                    }
+                    if (root.flags & NODE_COMPLETION) {
+                        if (wr) emit(root.slot, tid, 0, 0, rk);
+                        else count_n(root.slot, tid, 1);
+                    }
                     if (STATS) {
                         st[ST_ROOTS]++;
                         st[ST_BYTES] += 16 + (root_inner ? 16 : 0);
@@ -386,14 +471,14 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                         break;
                     }
                     --d;
-                    const uint32_t w0 = myfr[(d * kFrameWords + 0) * kLB];
-                    pos = myfr[(d * kFrameWords + 1) * kLB];
-                    tr_prev = myfr[(d * kFrameWords + 2) * kLB];
-                    lim = myfr[(d * kFrameWords + 3) * kLB];
-                    P.x = myfr[(d * kFrameWords + 4) * kLB];
-                    P.y = myfr[(d * kFrameWords + 5) * kLB];
-                    P.z = myfr[(d * kFrameWords + 6) * kLB];
-                    P.w = myfr[(d * kFrameWords + 7) * kLB];
+                    const uint32_t w0 = myfr[(d * FW + 0) * kLB];
+                    pos = myfr[(d * FW + 1) * kLB];
+                    tr_prev = myfr[(d * FW + 2) * kLB];
+                    lim = myfr[(d * FW + 3) * kLB];
+                    P.x = myfr[(d * FW + 4) * kLB];
+                    P.y = myfr[(d * FW + 5) * kLB];
+                    P.z = myfr[(d * FW + 6) * kLB];
+                    P.w = myfr[(d * FW + 7) * kLB];
                     node = w0 & 0xffffu;
                     g = w0 >> 16;
                     const LNode dn = s_nodes[node];
@@ -514,20 +599,25 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
             }
             if (hit == kNone) break;
             const LNode dn = s_nodes[hit];
+            uint32_t erk = 0;  // ENUM pass 2: input rank of the matched edge
+            if (wr) erk = glob ? __ldg(p.perm + (pos - 1))
+                               : __ldg((G.kind == ANCHOR_OUT ? p.out_rank : p.in_rank) + (pos - 1));
             if (dn.flags & NODE_COMPLETION) {
-                count_n(dn.slot, tid, 1);
+                if (wr) emit(dn.slot, tid, bpre, d, erk);
+                else count_n(dn.slot, tid, 1);
                 if (STATS) st[ST_MATCHES]++;
             }
             if (dn.flags & NODE_INNER) {
+                if (wr) myfr[(d * FW + kFrameWords) * kLB] = erk;
                 // the parent resumes at pos in its group (undo the early window close)
-                myfr[(d * kFrameWords + 0) * kLB] = node | (gc << 16);
-                myfr[(d * kFrameWords + 1) * kLB] = pos;
-                myfr[(d * kFrameWords + 2) * kLB] = tr_prev;
-                myfr[(d * kFrameWords + 3) * kLB] = lim;
-                myfr[(d * kFrameWords + 4) * kLB] = P.x;
-                myfr[(d * kFrameWords + 5) * kLB] = P.y;
-                myfr[(d * kFrameWords + 6) * kLB] = P.z;
-                myfr[(d * kFrameWords + 7) * kLB] = P.w;
+                myfr[(d * FW + 0) * kLB] = node | (gc << 16);
+                myfr[(d * FW + 1) * kLB] = pos;
+                myfr[(d * FW + 2) * kLB] = tr_prev;
+                myfr[(d * FW + 3) * kLB] = lim;
+                myfr[(d * FW + 4) * kLB] = P.x;
+                myfr[(d * FW + 5) * kLB] = P.y;
+                myfr[(d * FW + 6) * kLB] = P.z;
+                myfr[(d * FW + 7) * kLB] = P.w;
                 ++d;
                 if (dn.n_new >= 1) m2g_set<MAXV>(m2g, nv, e1);
                 if (dn.n_new == 2) m2g_set<MAXV>(m2g, nv + 1, e2);
@@ -559,6 +649,7 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
             const uint32_t hj = __shfl_sync(kFull, h, j);
             const uint32_t tpj = __shfl_sync(kFull, tr_prev, j);
             const uint32_t nvj = __shfl_sync(kFull, nv, j);
+            const uint32_t bj = __shfl_sync(kFull, bpre, j), dj = __shfl_sync(kFull, d, j);
             uint32_t mj[MAXV];
 #pragma unroll
             for (int k = 0; k < MAXV; k++) mj[k] = __shfl_sync(kFull, m2g[k], j);
@@ -574,7 +665,11 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                 for (uint32_t c = G.child_begin; c < G.child_end; ++c) {
                     const LNode dn = s_nodes[c];
                     const unsigned mc = __ballot_sync(kFull, w && cls == dn.want);
-                    if (lane == 0 && mc && (dn.flags & NODE_COMPLETION)) count_n(dn.slot, wbase + j, __popc(mc));
+                    if (wr) {
+                        if (w && cls == dn.want && (dn.flags & NODE_COMPLETION))
+                            emit(dn.slot, wbase + j, bj, dj,
+                                 __ldg((G.kind == ANCHOR_OUT ? p.out_rank : p.in_rank) + b + lane));
+                    } else if (lane == 0 && mc && (dn.flags & NODE_COMPLETION)) count_n(dn.slot, wbase + j, __popc(mc));
                     if (STATS && lane == 0) st[ST_MATCHES] += __popc(mc);
                 }
                 if (STATS) {
@@ -622,6 +717,12 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                     wstk[10 * kStackCap + slot] = R.w;
 #pragma unroll
                     for (int q = 0; q < MAXV; q++) wstk[(11 + q) * kStackCap + slot] = m2g[q];
+                    if (wr) {  // the task's base prefix: this search's prefix + its frames' edges
+                        wstk[(11 + MAXV) * kStackCap + slot] = bpre + d;
+                        for (uint32_t i = 0; i < bpre; i++) wstk[(12 + MAXV + i) * kStackCap + slot] = s_pre[i * kLB + tid];
+                        for (uint32_t i = 0; i < d; i++)
+                            wstk[(12 + MAXV + bpre + i) * kStackCap + slot] = myfr[(i * FW + kFrameWords) * kLB];
+                    }
                     g = g_end;  // handed out: pop back to the parent at the next step
                     fresh = false;
                     if (STATS) st[ST_OFFLOADS]++;
@@ -646,6 +747,14 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
     }
     // ---- counters: lanes -> block -> global, once per block
     __syncthreads();
+    if (ENUM && p.enum_pass == 1) {  // per-warp match counts (lane counters + their u64 overflow)
+        for (uint32_t sl = 0; sl < p.n_slots; sl++) {
+            unsigned long long v = s_cnt[sl * kLB + tid];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+            if (lane == 0) p.wcnt[(size_t)sl * n_warps + gwarp] = v + s_ebase[(tid >> 5) * p.n_slots + sl];
+        }
+    }
     if (LANECNT) {
         for (uint32_t s = (uint32_t)tid >> 5; s < p.n_slots; s += kLB / 32) {
             unsigned long long v = 0;

@@ -45,6 +45,7 @@ SIGNATURES = {
     "mayura_comine_ex": ([_P, _P, _u64, _u64, _P, _P, _int, _int, _P], _int),
     "mayura_comine_stats": ([_P, _P, _u64, _u64, _int, _P], _int),
     "mayura_partition_roots": ([_P, _i64, _u32, _P], _int),
+    "mayura_enumerate": ([_P, _P, _u64, _u64, _P, _P, _u64, _int, _P, _P], _int),
     "mayura_last_error": ([], ctypes.c_char_p),
     "mayura_version": ([], ctypes.c_char_p),
     "mayura_launch_count": ([], _u64),
@@ -202,6 +203,38 @@ def mayura_comine_stats(g: int, m: int, root_begin: int, root_end: int, independ
     return dict(zip(STATS_FIELDS, (int(x) for x in out)))
 
 
+def mayura_enumerate(g: int, m: int, root_begin: int, root_end: int, stream: Optional[int] = None,
+                     tuples_out=None, capacity_words: int = 0):
+    """Enumerate the matches of roots [root_begin, root_end).
+
+    tuples_out=None: the library writes into a host buffer sized by a first (size-query)
+    call; returns (counts, words) with words a uint32 numpy array.  tuples_out=<device
+    tensor of >= capacity_words int32/uint32>: written in place on the device; returns
+    (counts, words_needed).  Layout: include/mayura.h (motif q's tuples at W_q, len_q input
+    edge indices each)."""
+    k = mayura_mgtree_info(m)["n_motifs"]
+    counts = np.zeros(k, np.uint64)
+    need = ctypes.c_uint64(0)
+    if tuples_out is not None:
+        _check(_lib.mayura_enumerate(g, m, root_begin, root_end, stream, ctypes.c_void_p(tuples_out.data_ptr()),
+                                     int(capacity_words), 1, _ptr(counts), ctypes.byref(need)))
+        return [int(x) for x in counts], int(need.value)
+    _check(_lib.mayura_enumerate(g, m, root_begin, root_end, stream, None, 0, 0, _ptr(counts), ctypes.byref(need)))
+    words = np.zeros(max(int(need.value), 1), np.uint32)
+    _check(_lib.mayura_enumerate(g, m, root_begin, root_end, stream, _ptr(words), int(need.value), 0, _ptr(counts),
+                                 ctypes.byref(need)))
+    return [int(x) for x in counts], words[:int(need.value)]
+
+
+def split_tuples(counts: Sequence[int], lens: Sequence[int], words: np.ndarray) -> List[np.ndarray]:
+    """The enumeration buffer split per motif: a (count_q, len_q) array of input edge indices."""
+    out, w = [], 0
+    for c, L in zip(counts, lens):
+        out.append(np.asarray(words[w:w + c * L]).reshape(c, L))
+        w += c * L
+    return out
+
+
 def mayura_partition_roots(g: int, delta: int, n_parts: int) -> List[int]:
     out = np.zeros(n_parts + 1, np.uint64)
     _check(_lib.mayura_partition_roots(g, int(delta), int(n_parts), _ptr(out)))
@@ -245,6 +278,7 @@ class MGTree:
         self.info = mayura_mgtree_info(self.handle)
         self.n_motifs = self.info["n_motifs"]
         self.delta = delta
+        self.lens = [len(mo) for mo in motifs]
 
     def dump(self) -> str:
         return mayura_mgtree_dump(self.handle)
@@ -276,3 +310,10 @@ def mine_independent(graph: Graph, tree: MGTree, root_range: Optional[Tuple[int,
 def comine_stats(graph: Graph, tree: MGTree, root_range=None, independent: bool = False) -> dict:
     rb, re_ = root_range if root_range is not None else (0, graph.n_edges)
     return mayura_comine_stats(graph.handle, tree.handle, rb, re_, independent)
+
+
+def enumerate_matches(graph: Graph, tree: MGTree, root_range=None, stream: Optional[int] = None):
+    """Host enumeration: (counts, [per-motif (count, len) arrays of input edge indices])."""
+    rb, re_ = root_range if root_range is not None else (0, graph.n_edges)
+    counts, words = mayura_enumerate(graph.handle, tree.handle, rb, re_, stream)
+    return counts, split_tuples(counts, tree.lens, words)

@@ -1,0 +1,105 @@
+"""GPU parity of enumeration (mayura_enumerate, NEXT-3): the
+CUDA path's match lists vs the oracle's (oracle.enumerate_matches, pinned in
+test_enumerate_oracle.py).  Tuples are input edge indices in motif edge order; the
+order of the matches is unspecified, so each motif's list is compared as a sorted
+array (exact, every word), and the counts must equal mayura_comine's."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def M():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2507_14813_b200 as M
+    return M
+
+
+def _sorted_rows(a):
+    a = np.asarray(a, dtype=np.int64)
+    if a.size == 0:
+        return a.reshape(0, a.shape[1] if a.ndim == 2 else 0)
+    return a[np.lexsort(a.T[::-1])]
+
+
+def check(M, oracle_mod, src, dst, t, V, motifs, delta, root_range=None):
+    g = M.Graph(src, dst, t, V, device=0)
+    tree = M.MGTree(motifs, delta)
+    counts, lists = M.enumerate_matches(g, tree, root_range)
+    assert counts == M.comine(g, tree, root_range)
+    for q, mo in enumerate(motifs):
+        exp = oracle_mod.enumerate_matches(src, dst, t, V, mo, delta, root_range)
+        got = lists[q]
+        assert got.shape == exp.shape, (q, mo, got.shape, exp.shape)
+        assert np.array_equal(_sorted_rows(got), _sorted_rows(exp)), (q, mo)
+    g.close()
+    tree.close()
+    return counts
+
+
+def test_enumerate_fuzz_groups(M, oracle_mod):
+    """Random groups of 1-5 motifs (<= 4 edges, some prefix-disconnected: GLOBAL anchor)
+    on tie-heavy multigraphs with self-loops."""
+    nz = 0
+    for seed in range(60):
+        rng = np.random.default_rng(500 + seed)
+        V = int(rng.integers(3, 25))
+        src, dst, t, V = synth.random_graph(500 + seed, V, int(rng.integers(1, 250)), int(rng.integers(5, 150)))
+        motifs = [synth.random_motif(seed * 31 + j, int(rng.integers(1, 5)), int(rng.integers(2, 6)))
+                  for j in range(int(rng.integers(1, 6)))]
+        nz += sum(1 for c in check(M, oracle_mod, src, dst, t, V, motifs, int(rng.integers(0, 60))) if c)
+    assert nz > 60
+
+
+def test_enumerate_hubs_warp_help_and_donation(M, oracle_mod):
+    """Adjacency lists of 10^3-10^4 entries: long leaf windows are scanned by the whole
+    warp (tuples written by the helping lanes) and long searches are split into tasks
+    (their prefixes travel with the task)."""
+    for seed in range(3):
+        src, dst, t, V = synth.random_graph(90 + seed, 5 + seed, 6_000, 2_000 + 1000 * seed, 0.01)
+        motifs = synth.group(synth.GROUP_C2) + [synth.MOTIFS["recip2"], synth.MOTIFS["repeat2"]]
+        check(M, oracle_mod, src, dst, t, V, motifs, 8 + 4 * seed)
+
+
+def test_enumerate_c1_full_and_ranges(M, oracle_mod):
+    cfg = synth.CONFIGS["C1"]
+    src, dst, t, V = cfg.graph()
+    counts = check(M, oracle_mod, src, dst, t, V, cfg.group(), cfg.delta)
+    assert all(c > 0 for c in counts)
+    E = len(src)
+    check(M, oracle_mod, src, dst, t, V, cfg.group(), cfg.delta, (E // 3, E // 3 + 2500))
+
+
+def test_enumerate_duplicates_one_edge_and_prefix_motifs(M, oracle_mod):
+    """Duplicate motifs (reading R10) get identical lists; a 1-edge motif lists every
+    non-self-loop edge; a motif that is a prefix of another (an inner completion node)."""
+    src, dst, t, V = synth.random_graph(7, 12, 800, 300, 0.05)
+    motifs = [[(0, 1), (1, 2), (2, 0)], [(5, 6), (6, 9), (9, 5)], [(0, 1)], [(0, 1), (1, 2)],
+              [(0, 1), (1, 2), (2, 3)], [(0, 1), (2, 3)]]
+    check(M, oracle_mod, src, dst, t, V, motifs, 40)
+
+
+def test_enumerate_device_output_and_capacity(M, oracle_mod):
+    import torch
+    cfg = synth.CONFIGS["C1"]
+    src, dst, t, V = cfg.graph()
+    g = M.Graph(src, dst, t, V, device=0)
+    tree = M.MGTree(cfg.group(), cfg.delta)
+    host_counts, words = M.mayura_enumerate(g.handle, tree.handle, 0, g.n_edges)
+    need = len(words)
+    buf = torch.zeros(need, dtype=torch.int32, device="cuda:0")
+    dev_counts, need2 = M.mayura_enumerate(g.handle, tree.handle, 0, g.n_edges, None, buf, need)
+    assert dev_counts == host_counts and need2 == need
+    dev = buf.cpu().numpy().view(np.uint32)
+    for a, b in zip(M.split_tuples(host_counts, tree.lens, words), M.split_tuples(dev_counts, tree.lens, dev)):
+        assert np.array_equal(_sorted_rows(a), _sorted_rows(b))
+    small = torch.zeros(max(need - 1, 1), dtype=torch.int32, device="cuda:0")
+    with pytest.raises(M.MayuraError):
+        M.mayura_enumerate(g.handle, tree.handle, 0, g.n_edges, None, small, need - 1)
+    g.close()
+    tree.close()

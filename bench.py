@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-indep", action="store_true")
+    ap.add_argument("--no-enum", action="store_true", help="skip the enumeration (NEXT-3) leg")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no extras")
     return ap.parse_args()
@@ -193,6 +194,50 @@ def run_reference(args, cfg, world, rank):
     print(json.dumps(out), flush=True)
 
 
+def enumeration_leg(M, g, tree, cfg, src, dst, t, V, sp, stream, st, peak, got, reps: int = 3):
+    """NEXT-3: mayura_enumerate into a device buffer (two kernel passes + a CUB scan + the
+    tuple writes), event-timed per call on the launching stream (the call synchronises once
+    in the middle to size the output).  Algorithmic bytes = 2 x the counting pass's B_alg
+    (both passes traverse) + 4 B per tuple word written.  Parity vs the oracle's match lists
+    (sorted per motif, every word) when the graph is small enough for the oracle."""
+    import numpy as np
+    import torch
+    host_counts, need = M.mayura.mayura_enumerate_size(g.handle, tree.handle, 0, g.n_edges, sp)
+    buf = torch.empty(max(need, 1), dtype=torch.int32, device=stream.device)
+    M.mayura_enumerate(g.handle, tree.handle, 0, g.n_edges, sp, buf, need)  # warm-up
+    ms = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        c, _ = M.mayura_enumerate(g.handle, tree.handle, 0, g.n_edges, sp, buf, need)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t_ms = statistics.median(ms)
+    matches = sum(host_counts)
+    b_alg = 2 * st["bytes_alg"] + 4 * need
+    parity = None
+    if len(src) <= 400_000:
+        import oracle
+        dev_words = buf[:need].cpu().numpy().view(np.uint32)
+        ok = True
+        for a, mo in zip(M.split_tuples(host_counts, tree.lens, dev_words), cfg.group()):
+            b = oracle.enumerate_matches(src, dst, t, V, mo, cfg.delta)
+            a = np.asarray(a, np.int64)
+            b = np.asarray(b, np.int64)
+            if a.shape != b.shape or not np.array_equal(a[np.lexsort(a.T[::-1])], b[np.lexsort(b.T[::-1])]):
+                ok = False
+        parity = "exact (every tuple, sorted per motif)" if ok else "MISMATCH"
+    return {"matches": matches, "words": need, "ms": t_ms, "matches_per_s": matches / (t_ms * 1e-3),
+            "counts_equal_comine": c == got and host_counts == got,
+            "roofline": {"bound": "hbm", "achieved": b_alg / (t_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": b_alg / (t_ms * 1e-3) / 1e9 / peak, "bytes_alg": b_alg,
+                         "note": "2 traversal passes (B_alg each) + 4 B per output word; includes the mid-call "
+                                 "host sync that sizes the output"},
+            "parity_vs_oracle": parity,
+            "path": "mayura_enumerate(device output): count pass per warp, CUB scan, write pass"}
+
+
 def main():
     args = parse()
     world, rank, local = dist_env()
@@ -332,6 +377,10 @@ def main():
                "path": "mayura_load_graph(pinned host src/dst/t -> H2D, graph build on the GPU) + "
                        "mayura_comine + D2H of the counts"}
 
+    enum = None
+    if world == 1 and not args.no_enum and not args.profile:
+        enum = enumeration_leg(M, g, tree, cfg, src, dst, t, V, sp, stream, st, peak, got)
+
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -356,7 +405,7 @@ def main():
                "gpu_launches_detail": "mayura_launch_count() over the timed steps x ranks: per step "
                                       "window_end_kernel + expand_kernel + long_kernel + comine_lane_kernel",
                "roofline": roofline, "clocks": clocks, "e2e": e2e, "independent_gpu": indep,
-               "cpu_baseline": cpu, "search_stats": st}
+               "cpu_baseline": cpu, "search_stats": st, "enumeration": enum}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()

@@ -209,6 +209,20 @@ mayura_status mayura_enumerate(mayura_graph g, mayura_mgtree m, uint64_t root_be
                                uint64_t capacity_words, int tuples_on_device,
                                uint64_t *counts_out, uint64_t *words_needed);
 
+/* mayura_comine_heuristic -- the paper's rule for whether co-mining the group beats
+ * mining each motif on its own (§6 "Heuristic for Co-Mining"; the
+ * listing itself is figure-only, reading R18): co-mine if the graph is
+ * bipartite (co-mining "has always resulted in a performance improvement" there) or the
+ * group's Similarity Metric is >= 0.44.
+ *   use_comine : 1 = co-mine, 0 = mine independently.    (each output may be NULL)
+ *   bipartite  : 1 if the underlying undirected graph is 2-colourable (a self-loop is
+ *                an odd cycle), else 0.
+ *   sm         : the group's Similarity Metric (as mayura_mgtree_info).
+ * Host computation (union-find over the edges); a device-built graph's edge arrays are
+ * downloaded once.  Errors: E_INVALID (NULL handle), E_OOM, E_CUDA. */
+mayura_status mayura_comine_heuristic(mayura_graph g, mayura_mgtree m, int *use_comine,
+                                      int *bipartite, double *sm);
+
 /* ------------------------------------------------------------ multi-GPU ---
  * mayura_partition_roots -- split [0, E) into n_parts contiguous root ranges
  * (timestamp ranges) of balanced estimated work (proxy: 1 + number of edges in

@@ -176,3 +176,65 @@ extern "C" mayura_status mayura_partition_roots(mayura_graph g, int64_t delta, u
     bounds_out[n_parts] = E;
     return MAYURA_OK;
 }
+
+// NEXT-4: the paper's co-mining heuristic (§6 "Heuristic for Co-Mining";
+// its Listing "heuristic.py" is figure-only, reading R18): co-mining always paid off on
+// bipartite graphs, and otherwise needs a Similarity Metric of at least 0.44.
+// Bipartiteness of the underlying undirected graph: union-find with parity over the edges
+// (an edge joins opposite colours; a self-loop is an odd cycle).
+namespace mayura {
+namespace {
+bool graph_bipartite(const std::vector<uint32_t> &src, const std::vector<uint32_t> &dst, uint32_t V) {
+    std::vector<uint32_t> parent(V), par(V, 0);  // par: colour relative to the parent
+    for (uint32_t v = 0; v < V; v++) parent[v] = v;
+    auto find = [&](uint32_t x, uint32_t &colour) {
+        uint32_t c = 0, r = x;
+        while (parent[r] != r) {
+            c ^= par[r];
+            r = parent[r];
+        }
+        // path compression: point x's chain at the root with its colour relative to it
+        uint32_t cx = c;
+        while (parent[x] != r && parent[x] != x) {
+            const uint32_t nx = parent[x], px = par[x];
+            parent[x] = r;
+            par[x] = cx;
+            cx ^= px;
+            x = nx;
+        }
+        colour = c;
+        return r;
+    };
+    for (size_t i = 0; i < src.size(); i++) {
+        const uint32_t a = src[i], b = dst[i];
+        if (a == b) return false;
+        uint32_t ca = 0, cb = 0;
+        const uint32_t ra = find(a, ca), rb = find(b, cb);
+        if (ra == rb) {
+            if (ca == cb) return false;
+        } else {
+            parent[ra] = rb;
+            par[ra] = ca ^ cb ^ 1u;  // colour(a) != colour(b)
+        }
+    }
+    return true;
+}
+}  // namespace
+}  // namespace mayura
+
+extern "C" mayura_status mayura_comine_heuristic(mayura_graph g, mayura_mgtree m, int *use_comine, int *bipartite,
+                                                 double *sm) {
+    clear_error();
+    if (!g || !m) return fail(MAYURA_E_INVALID, "mayura_comine_heuristic: NULL handle");
+    if (mayura_status s = ensure_host(g)) return s;
+    bool bip;
+    try {
+        bip = graph_bipartite(g->src, g->dst, g->V);
+    } catch (const std::bad_alloc &) {
+        return fail(MAYURA_E_OOM, "mayura_comine_heuristic: out of host memory");
+    }
+    if (bipartite) *bipartite = bip ? 1 : 0;
+    if (sm) *sm = m->sm;
+    if (use_comine) *use_comine = (bip || m->sm >= 0.44) ? 1 : 0;
+    return MAYURA_OK;
+}

@@ -46,6 +46,7 @@ SIGNATURES = {
     "mayura_comine_stats": ([_P, _P, _u64, _u64, _int, _P], _int),
     "mayura_partition_roots": ([_P, _i64, _u32, _P], _int),
     "mayura_enumerate": ([_P, _P, _u64, _u64, _P, _P, _u64, _int, _P, _P], _int),
+    "mayura_comine_heuristic": ([_P, _P, _P, _P, _P], _int),
     "mayura_last_error": ([], ctypes.c_char_p),
     "mayura_version": ([], ctypes.c_char_p),
     "mayura_launch_count": ([], _u64),
@@ -226,6 +227,15 @@ def mayura_enumerate(g: int, m: int, root_begin: int, root_end: int, stream: Opt
     return [int(x) for x in counts], words[:int(need.value)]
 
 
+def mayura_enumerate_size(g: int, m: int, root_begin: int, root_end: int, stream: Optional[int] = None):
+    """Size query of mayura_enumerate (tuples_out = NULL): (counts, words needed)."""
+    k = mayura_mgtree_info(m)["n_motifs"]
+    counts = np.zeros(k, np.uint64)
+    need = ctypes.c_uint64(0)
+    _check(_lib.mayura_enumerate(g, m, root_begin, root_end, stream, None, 0, 0, _ptr(counts), ctypes.byref(need)))
+    return [int(x) for x in counts], int(need.value)
+
+
 def split_tuples(counts: Sequence[int], lens: Sequence[int], words: np.ndarray) -> List[np.ndarray]:
     """The enumeration buffer split per motif: a (count_q, len_q) array of input edge indices."""
     out, w = [], 0
@@ -233,6 +243,13 @@ def split_tuples(counts: Sequence[int], lens: Sequence[int], words: np.ndarray) 
         out.append(np.asarray(words[w:w + c * L]).reshape(c, L))
         w += c * L
     return out
+
+
+def mayura_comine_heuristic(g: int, m: int) -> dict:
+    """The paper's co-mining heuristic: {use_comine, bipartite, sm}."""
+    use, bip, sm = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_double(0.0)
+    _check(_lib.mayura_comine_heuristic(g, m, ctypes.byref(use), ctypes.byref(bip), ctypes.byref(sm)))
+    return {"use_comine": bool(use.value), "bipartite": bool(bip.value), "sm": sm.value}
 
 
 def mayura_partition_roots(g: int, delta: int, n_parts: int) -> List[int]:

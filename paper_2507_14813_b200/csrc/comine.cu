@@ -234,10 +234,10 @@ KernelKind kernel_kind() {
     return (KernelKind)v;
 }
 // hybrid: a root is split breadth-first only if one of its root-node windows has >= this
-// many entries.  Measured (profiles/README.md): graphs that fit in L2 gain from splitting
-// every root (frontier records are cheap there; C1/C2), DRAM-resident graphs from splitting
-// only roots with a window of >= 16 entries (C3 9.2 -> 6.2 ms, C4 110 -> 103 ms).
-// MAYURA_HEAVY_MIN overrides (0 = split every root).
+// many entries; the breadth-first level lists the light ones for the depth-first kernel.
+// Measured sweep (profiles/README.md r04, H in {0,4,8,16,32}): graphs that fit in L2 are
+// best at 8 (C2 0.575 ms at 0 -> 0.524 at 8), DRAM-resident graphs at 16 (C3 8.3 ms at 0 ->
+// 4.79 at 16).  MAYURA_HEAVY_MIN overrides (0 = split every root).
 uint32_t heavy_min(const mayura_graph_s *g) {
     static int v = -2;
     if (v == -2) {
@@ -247,7 +247,7 @@ uint32_t heavy_min(const mayura_graph_s *g) {
     if (v >= 0) return (uint32_t)v;
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
-    return g->graph_bytes <= (uint64_t)l2 ? 0u : 16u;
+    return g->graph_bytes <= (uint64_t)l2 ? 8u : 16u;
 }
 // hybrid: breadth-first levels before the depth-first lane kernel (MAYURA_HYBRID_LEVELS)
 uint32_t hybrid_levels() {

@@ -186,14 +186,14 @@ __device__ __forceinline__ void make_child(const BParams &p, const DGroup &G, co
 // next frontier is full): one thread, frames in local memory.
 template <int MAXV, bool STATS>
 __device__ __noinline__ void dfs(const BParams &p, const lane::LNode *nodes, const DGroup *groups, PM<MAXV> x,
-                                 Ctx &c) {
+                                 Ctx &c, uint32_t g_first = kNone) {  // g_first: start at this group of x
     struct Fr {
         uint32_t node, nv, g, pos, lim, tr_prev;
         uint4 P;
         uint32_t m2g[MAXV];
     } fr[kMaxLevels];
     int d = 0;
-    uint32_t g = nodes[x.node].group_begin, pos = 0, lim = kNone;
+    uint32_t g = g_first != kNone ? g_first : nodes[x.node].group_begin, pos = 0, lim = kNone;
     bool scan = false;
     for (;;) {
         const lane::LNode xn = nodes[x.node];

@@ -39,6 +39,7 @@ enum { LB_ROOT = 0, LB_N = 8 };
 
 #include "lane.cuh"
 #include "bfs.cuh"
+#include "flat.cuh"
 
 // a2: hi[r] = (last edge id e with t[e] <= t[r] + delta), by galloping from r (windows
 // are short) then binary search.  Also zeroes the load-balancer words and the output
@@ -223,15 +224,13 @@ cudaError_t launch_lane(const lane::LParams &p, uint32_t max_vertices, bool stat
     return launch_lane_v<16>(p, stats, generic, s, sms);
 }
 
-// Kernel choice (MAYURA_KERNEL): "hybrid" (default), "lane", "bfs".
-enum KernelKind { K_HYBRID = 0, K_LANE = 1, K_BFS = 2 };
-KernelKind kernel_kind() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("MAYURA_KERNEL");
-        v = (e && std::strcmp(e, "lane") == 0) ? K_LANE : (e && std::strcmp(e, "bfs") == 0) ? K_BFS : K_HYBRID;
-    }
-    return (KernelKind)v;
+// Kernel choice (MAYURA_KERNEL): "hybrid" (default), "lane", "bfs", "flat".
+enum KernelKind { K_HYBRID = 0, K_LANE = 1, K_BFS = 2, K_FLAT = 3 };
+KernelKind kernel_kind() {  // read per call (tests switch forms within one process)
+    const char *e = getenv("MAYURA_KERNEL");
+    return (e && std::strcmp(e, "lane") == 0) ? K_LANE
+           : (e && std::strcmp(e, "bfs") == 0) ? K_BFS
+           : (e && std::strcmp(e, "flat") == 0) ? K_FLAT : K_HYBRID;
 }
 // hybrid: a root is split breadth-first only if one of its root-node windows has >= this
 // many entries; the breadth-first level lists the light ones for the depth-first kernel.
@@ -310,6 +309,31 @@ cudaError_t launch_bfs(bfs::BParams &p, uint32_t max_vertices, uint32_t levels, 
     return launch_bfs_v<16>(p, levels, bufs, ctl, seg_cap, stats, s, sms);
 }
 
+// ---- flat (level-synchronous, entry-parallel): per level a window pass and an entry pass
+template <int MAXV, bool L0>
+cudaError_t launch_flat_level(const flat::FParams &f, cudaStream_t s, int sms) {
+    const size_t smem = bfs::smem_bytes(f.b.n_nodes, f.b.n_groups, f.b.n_slots, flat::kTB);
+    for (int pass = 0; pass < 2; pass++) {
+        auto kern = pass == 0 ? flat::flat_win_kernel<MAXV, L0> : flat::flat_entry_kernel<MAXV, L0>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, flat::kTB, smem);
+        if (e != cudaSuccess) return e;
+        uint32_t grid = (uint32_t)(sms * (per_sm > 0 ? per_sm : 1));
+        if (L0 && pass == 0) grid = std::max(1u, std::min(grid, (f.b.n_roots + flat::kTB - 1) / flat::kTB));
+        kern<<<grid, flat::kTB, smem, s>>>(f);
+        count_launch();
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+template <int MAXV>
+cudaError_t launch_flat_v(bfs::BParams p, uint32_t levels, uint32_t *bufs[2], uint32_t *ctl, uint32_t seg_cap,
+                          uint4 *win, uint32_t win_cap, cudaStream_t s, int sms);
+
 uint32_t rec_words(uint32_t max_vertices) {
     const uint32_t mv = max_vertices <= 4 ? 4 : max_vertices <= 6 ? 6 : max_vertices <= 8 ? 8 : 16;
     return (8 + mv + 3) & ~3u;
@@ -366,6 +390,51 @@ mayura_status ensure_bfs_buffers(mayura_graph_s *g, uint32_t words, int nbufs) {
         CK((cudaError_t)dmalloc((void **)&g->d_light, sizeof(uint32_t) * ((size_t)g->E + 32)), "cudaMalloc(light roots)");
         g->device_bytes += sizeof(uint32_t) * ((size_t)g->E + 32);
     }
+    return MAYURA_OK;
+}
+
+template <int MAXV>
+cudaError_t launch_flat_v(bfs::BParams p, uint32_t levels, uint32_t *bufs[2], uint32_t *ctl, uint32_t seg_cap,
+                          uint4 *win, uint32_t win_cap, cudaStream_t s, int sms) {
+    for (uint32_t L = 0; L < levels; L++) {
+        p.in.data = L ? bufs[(L - 1) & 1] : nullptr;
+        p.in.cnt = L ? ctl + (L - 1) * kCtlWords : nullptr;
+        p.in.seg_cap = seg_cap;
+        p.out.data = bufs[L & 1];
+        p.out.cnt = ctl + L * kCtlWords;
+        p.out.seg_cap = seg_cap;
+        flat::FParams f;
+        f.b = p;
+        f.win = win;
+        f.win_cnt = ctl + L * kCtlWords + bfs::kStripes;
+        f.cursor = ctl + L * kCtlWords + bfs::kStripes + 1;
+        f.win_cap = win_cap;
+        cudaError_t e = L == 0 ? launch_flat_level<MAXV, true>(f, s, sms) : launch_flat_level<MAXV, false>(f, s, sms);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_flat(const bfs::BParams &p, uint32_t max_vertices, uint32_t levels, uint32_t *bufs[2], uint32_t *ctl,
+                        uint32_t seg_cap, uint4 *win, uint32_t win_cap, cudaStream_t s, int sms) {
+    if (max_vertices <= 4) return launch_flat_v<4>(p, levels, bufs, ctl, seg_cap, win, win_cap, s, sms);
+    if (max_vertices <= 6) return launch_flat_v<6>(p, levels, bufs, ctl, seg_cap, win, win_cap, s, sms);
+    if (max_vertices <= 8) return launch_flat_v<8>(p, levels, bufs, ctl, seg_cap, win, win_cap, s, sms);
+    return launch_flat_v<16>(p, levels, bufs, ctl, seg_cap, win, win_cap, s, sms);
+}
+
+// Window-piece buffer of the flat form: 8 pieces per edge, >= 2^20, <= 15 % of free memory.
+mayura_status ensure_flat_win(mayura_graph_s *g) {
+    if (g->d_flat_win) return MAYURA_OK;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    uint64_t cap = std::max<uint64_t>(1u << 20, std::min<uint64_t>(8 * g->E, (uint64_t)(free_b * 0.15) / 16));
+    cap = std::min<uint64_t>(cap, 0xFFFFFFFFull);
+    if (const char *e = getenv("MAYURA_FLAT_WIN_CAP")) cap = (uint64_t)std::max(1L, atol(e));  // test hook
+    CK((cudaError_t)dmalloc((void **)&g->d_flat_win, 16 * cap), "cudaMalloc(window pieces)");
+    g->flat_win_cap = (uint32_t)cap;
+    g->device_bytes += 16 * cap;
+    g->fresh_alloc = true;
     return MAYURA_OK;
 }
 
@@ -521,6 +590,22 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
     uint32_t levels = 0;  // breadth-first levels before the depth-first phase
     if (kind == K_HYBRID) levels = std::min(hybrid_levels(), dt.max_edges > 2 ? dt.max_edges - 2 : 0u);
     if (kind == K_BFS) levels = dt.max_edges > 1 ? dt.max_edges - 1 : 1;
+    if (kind == K_FLAT && !st) {  // (the instrumented run uses the hybrid's counters)
+        const uint32_t fl = dt.max_edges > 1 ? dt.max_edges - 1 : 1;
+        mayura_status bs = ensure_bfs_buffers(g, words, 2);
+        if (bs != MAYURA_OK) return bs;
+        bs = ensure_flat_win(g);
+        if (bs != MAYURA_OK) return bs;
+        uint32_t *ctl = g->d_bfs_ctl;
+        CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * (kCtlWords * bfs::kMaxLevels + 16), s), "cudaMemsetAsync(ctl)");
+        bfs::BParams b = bfs_params(g, dt, r0, n_roots, counts, nullptr, 0u);
+        uint32_t *bufs[2] = {g->d_bfs[0], g->d_bfs[1]};
+        CK(launch_flat(b, dt.max_vertices, fl, bufs, ctl, g->bfs_seg_cap, reinterpret_cast<uint4 *>(g->d_flat_win),
+                       g->flat_win_cap, s, sms),
+           "flat pass launch");
+        return MAYURA_OK;
+    }
+    if (kind == K_FLAT) levels = std::min(hybrid_levels(), dt.max_edges > 2 ? dt.max_edges - 2 : 0u);
     lane::LParams q = lane_params(g, dt, r0, n_roots, lb, counts, stats, st);
     if (levels > 0) {
         mayura_status bs = ensure_bfs_buffers(g, words, levels >= 2 ? 2 : 1);
@@ -603,8 +688,10 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
         uint32_t mv = tabs[0].max_vertices;
         for (size_t i = 1; i < tabs.size(); i++) mv = std::max(mv, tabs[i].max_vertices);
         if (kernel_kind() != K_LANE && n_roots > 0) {
-            const uint32_t lv = kernel_kind() == K_BFS ? 2u : std::min(hybrid_levels(), 2u);
+            const uint32_t lv = kernel_kind() == K_BFS || kernel_kind() == K_FLAT ? 2u : std::min(hybrid_levels(), 2u);
             if (lv > 0) st = ensure_bfs_buffers(g, rec_words(mv), lv >= 2 ? 2 : 1);
+            if (st != MAYURA_OK) return st;
+            if (kernel_kind() == K_FLAT) st = ensure_flat_win(g);
             if (st != MAYURA_OK) return st;
         }
         if (g->fresh_alloc) {
@@ -797,7 +884,7 @@ void free_device(mayura_graph_s *g) {
     void *ptrs[] = {g->d_src, g->d_dst, g->d_tr, g->d_hi, g->d_t, g->d_out_off, g->d_in_off, g->d_out_ent,
                     g->d_in_ent, g->d_eptr, g->d_out_ptr, g->d_in_ptr, g->d_perm, g->d_queue, g->d_counts,
                     g->d_stats, g->d_dbg, g->d_bfs[0], g->d_bfs[1], g->d_bfs_ctl, g->d_bfs_long, g->d_light,
-                    g->d_out_rank, g->d_in_rank, g->d_enum};
+                    g->d_out_rank, g->d_in_rank, g->d_enum, g->d_flat_win};
     cudaDeviceSynchronize();  // no queued work may still use the memory returned to the pool
     for (void *p : ptrs) dfree(p);
     cudaStreamSynchronize(0);

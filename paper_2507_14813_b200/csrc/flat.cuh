@@ -1,0 +1,217 @@
+// flat.cuh -- level-synchronous, entry-parallel co-mining (MAYURA_KERNEL=flat), included by
+// comine.cu after bfs.cuh (it reuses bfs:: records, counters, window starts and the dfs fallback).
+//
+// Algorithm 3 "Co-Mining" advanced one MG-Tree level at a time over ALL
+// partial matches of the level, in two kernels per level k:
+//   flat_win_kernel    thread per partial match x of F_k (F_0 = the root edges): the exact
+//                      window [lo, lo + n) of every anchor group of node(x) (Algo 1 l.210-214:
+//                      entries with tr_prev < tr <= hi(root)), located by successor pointers /
+//                      search and a galloping search for its end; windows are appended as
+//                      pieces of <= kPiece entries {x, group, start, n} (warp-aggregated).
+//   flat_entry_kernel  warp per 32 pieces, LANE PER WINDOW ENTRY: a warp-wide prefix sum of the
+//                      pieces' lengths assigns entries to lanes 32 at a time, so every lane
+//                      tests one candidate (class against the owner's m2g, at most one child
+//                      per class -- Algo 1 l.219 + R4); completion children are counted
+//                      (Algo 3 l.661), inner children appended to F_{k+1} (warp-aggregated).
+// The depth-first lane kernel spends most of its issue slots on a divergent per-lane state
+// machine (profiles/README.md r03: 22 warp instructions per window entry, 13.6 active lanes);
+// here the per-entry work is straight-line code on full warps.  A full window or frontier
+// buffer never loses work: the thread mines the rest of that subtree depth-first (bfs::dfs).
+// Counts are identical to every other kernel form.
+
+namespace flat {
+
+constexpr int kTB = 256;
+constexpr uint32_t kPiece = 64;  // entries per window piece (bounds one warp-round batch)
+
+struct FParams {
+    bfs::BParams b;      // graph, table, frontier in (F_k) / out (F_{k+1}), counts
+    uint4 *win;          // window pieces {x, group, start, n}; x = root edge id (k = 0) or F_k index
+    uint32_t *win_cnt;   // [0] pieces appended at this level (may exceed win_cap)
+    uint32_t *cursor;    // [0] pieces taken by the entry pass
+    uint32_t win_cap;
+};
+
+// first position q in [lo, sent] with ent[q].x > key; ent[sent] is the list's sentinel (> any
+// key).  Galloping from lo: windows are short, so this costs one or two dependent loads.
+__device__ __forceinline__ uint32_t first_gt(const uint2 *ent, uint32_t lo, uint32_t sent, uint32_t key) {
+    uint32_t a = lo, b = sent, step = 1;
+    while (a < b) {
+        const uint32_t probe = min(b, a + step - 1);
+        if (__ldg(&ent[probe].x) > key) {
+            b = probe;
+            break;
+        }
+        a = probe + 1;
+        step <<= 1;
+    }
+    while (a < b) {
+        const uint32_t mid = a + ((b - a) >> 1);
+        if (__ldg(&ent[mid].x) > key) b = mid;
+        else a = mid + 1;
+    }
+    return a;
+}
+
+// The exact window of group G for partial match x: start and entry count.
+template <int MAXV>
+__device__ __forceinline__ uint32_t window(const bfs::BParams &p, const DGroup &G, const bfs::PM<MAXV> &x,
+                                           uint32_t &n, bfs::Ctx &c) {
+    uint32_t lim;
+    uint32_t lo = bfs::window_start<MAXV, false>(p, G, x, lim, c);
+    if (G.kind == ANCHOR_GLOBAL) {  // edge ids (tr_prev-tie-group end, hi(root)] (reading R6)
+        n = x.h + 1 > lo ? x.h + 1 - lo : 0;
+        return lo;
+    }
+    const uint2 *ent = (G.kind == ANCHOR_OUT) ? p.out_ent : p.in_ent;
+    const uint32_t *off = (G.kind == ANCHOR_OUT) ? p.out_off : p.in_off;
+    const uint32_t sent = __ldg(off + lane::m2g_get<MAXV>(x.m2g, G.anchor) + 1) - 1;
+    if (G.start >= START_R0 && G.start < START_SEARCH) lo = first_gt(ent, lo, sent, x.tr_prev);  // lower bound
+    n = first_gt(ent, lo, sent, x.h) - lo;
+    return lo;
+}
+
+template <int MAXV, bool L0>
+__global__ void __launch_bounds__(kTB) flat_win_kernel(const __grid_constant__ FParams f) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const bfs::BParams &p = f.b;
+    const bfs::Smem s = bfs::smem_setup(p, smem, L0);
+    bfs::Ctx c;
+    c.cnt = s.cnt + threadIdx.x;
+    c.stride = blockDim.x;
+    c.tot = s.tot;
+#pragma unroll
+    for (int i = 0; i < ST_N; i++) c.st[i] = 0;
+    c.em_next = c.em_end = 0;
+    const uint32_t n_items = L0 ? p.n_roots : s.pref[bfs::kStripes];
+    const lane::LNode root = s.nodes[0];
+    const uint32_t lane_id = threadIdx.x & 31;
+    for (uint32_t base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n_items;
+         base += gridDim.x * blockDim.x) {  // warp-uniform trip count (aggregated appends below)
+        const uint32_t item = base + lane_id;
+        bfs::PM<MAXV> x;
+        bool go = item < n_items;
+        uint32_t xid = item;
+        if (L0) {
+            xid = p.r0 + item;
+            if (go && !bfs::load_root<MAXV>(p, xid, x)) go = false;
+            if (go && (root.flags & NODE_COMPLETION)) bfs::count_add(c, root.slot, 1);
+            if (!(root.flags & NODE_INNER)) go = false;
+        } else if (go) {
+            bfs::load_rec<MAXV>(p, s.pref, item, x);
+            go = x.node != bfs::kHole;
+        }
+        const lane::LNode xn = s.nodes[go ? x.node : 0];
+        const uint32_t ng = go ? (uint32_t)(xn.group_end - xn.group_begin) : 0u;
+        const uint32_t maxg = __reduce_max_sync(kFull, ng);
+        bool fell = false;  // the window buffer was full: x's remaining groups were mined depth-first
+        for (uint32_t gi = 0; gi < maxg; gi++) {
+            const bool mine = gi < ng && !fell;
+            const uint32_t g = xn.group_begin + gi;
+            uint32_t lo = 0, n = 0;
+            if (mine) lo = window<MAXV>(p, s.groups[g], x, n, c);
+            const uint32_t np = (n + kPiece - 1) / kPiece;
+            uint32_t incl = np;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(kFull, incl, o);
+                if (lane_id >= (uint32_t)o) incl += v;
+            }
+            const uint32_t total = __shfl_sync(kFull, incl, 31);
+            uint32_t wb = 0;
+            if (lane_id == 0 && total) wb = atomicAdd(f.win_cnt, total);
+            wb = __shfl_sync(kFull, wb, 0);
+            const uint32_t at = wb + incl - np;
+            if (np) {
+                if (at + np <= f.win_cap) {
+                    for (uint32_t q = 0; q < np; q++)
+                        f.win[at + q] = make_uint4(xid, g, lo + q * kPiece, min(kPiece, n - q * kPiece));
+                } else {  // no room: empty the reserved slots that exist, mine the rest in place
+                    for (uint32_t q = at; q < at + np && q < f.win_cap; q++) f.win[q] = make_uint4(0, 0, 0, 0);
+                    atomicAdd(p.fallback, 1u);
+                    bfs::dfs<MAXV, false>(p, s.nodes, s.groups, x, c, g);
+                    fell = true;
+                }
+            }
+        }
+    }
+    bfs::flush<false>(p, s, c);
+}
+
+template <int MAXV, bool L0>
+__global__ void __launch_bounds__(kTB) flat_entry_kernel(const __grid_constant__ FParams f) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const bfs::BParams &p = f.b;
+    const bfs::Smem s = bfs::smem_setup(p, smem, L0);
+    bfs::Ctx c;
+    c.cnt = s.cnt + threadIdx.x;
+    c.stride = blockDim.x;
+    c.tot = s.tot;
+#pragma unroll
+    for (int i = 0; i < ST_N; i++) c.st[i] = 0;
+    c.em_next = c.em_end = 0;
+    const uint32_t lane_id = threadIdx.x & 31;
+    const uint32_t n_win = min(*(volatile uint32_t *)f.win_cnt, f.win_cap);
+    for (;;) {
+        uint32_t wb = 0;
+        if (lane_id == 0) wb = atomicAdd(f.cursor, 32u);
+        wb = __shfl_sync(kFull, wb, 0);
+        if (wb >= n_win) break;
+        const uint32_t wi = wb + lane_id;
+        const uint4 w = wi < n_win ? f.win[wi] : make_uint4(0, 0, 0, 0);
+        const uint32_t n = w.w;
+        bfs::PM<MAXV> x;
+        x.node = 0; x.nv = 0; x.root = 0; x.h = 0;
+#pragma unroll
+        for (int k = 0; k < MAXV; k++) x.m2g[k] = kNone;
+        if (n) {
+            if (L0) bfs::load_root<MAXV>(p, w.x, x);
+            else bfs::load_rec<MAXV>(p, s.pref, w.x, x);
+        }
+        uint32_t incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(kFull, incl, o);
+            if (lane_id >= (uint32_t)o) incl += v;
+        }
+        const uint32_t excl = incl - n, T = __shfl_sync(kFull, incl, 31);
+        for (uint32_t rb = 0; rb < T; rb += 32) {
+            const uint32_t j = rb + lane_id;
+            const bool act = j < T;
+            uint32_t o = 0;  // owner: the first lane whose inclusive sum exceeds j
+#pragma unroll
+            for (uint32_t st = 16; st; st >>= 1)
+                if (__shfl_sync(kFull, incl, o + st - 1) <= j) o += st;
+            o = min(o, 31u);
+            bfs::PM<MAXV> xo;
+#pragma unroll
+            for (int k = 0; k < MAXV; k++) xo.m2g[k] = __shfl_sync(kFull, x.m2g[k], o);
+            xo.node = __shfl_sync(kFull, x.node, o);
+            xo.nv = __shfl_sync(kFull, x.nv, o);
+            xo.root = __shfl_sync(kFull, x.root, o);
+            xo.h = __shfl_sync(kFull, x.h, o);
+            const uint32_t g = __shfl_sync(kFull, w.y, o);
+            const uint32_t pos = __shfl_sync(kFull, w.z, o) + (j - __shfl_sync(kFull, excl, o));
+            uint32_t ch = kNone, etr = 0, e1 = 0, e2 = 0;
+            DGroup G = s.groups[act ? g : 0];
+            if (act) {
+                bfs::load_entry(p, G, pos, kNone, etr, e1, e2);
+                ch = bfs::find_child(s.nodes, G, bfs::entry_class<MAXV>(G, xo.m2g, e1, e2));
+            }
+            bool inner = false;
+            if (ch != kNone) {
+                const lane::LNode dn = s.nodes[ch];
+                if (dn.flags & NODE_COMPLETION) bfs::count_add(c, dn.slot, 1);
+                inner = (dn.flags & NODE_INNER) != 0;
+            }
+            if (inner) {
+                bfs::PM<MAXV> y;
+                bfs::make_child<MAXV>(p, G, s.nodes[ch], ch, xo, pos, etr, e1, e2, y);
+                bfs::emit<MAXV, false, false>(p, s.nodes, s.groups, y, c);  // warp-aggregated append
+            }
+        }
+    }
+    bfs::flush<false>(p, s, c);
+}
+
+}  // namespace flat

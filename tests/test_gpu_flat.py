@@ -1,0 +1,67 @@
+"""GPU parity of the level-synchronous, entry-parallel kernel form (MAYURA_KERNEL=flat,
+csrc/flat.cuh) vs the oracle: random groups, hub lists, the C1 workload, the 87-motif
+3-edge family (every anchor kind incl. GLOBAL), and forced overflow of the window-piece
+and frontier buffers (the depth-first fallback must keep counts exact)."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture()
+def M(monkeypatch):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    monkeypatch.setenv("MAYURA_KERNEL", "flat")
+    import paper_2507_14813_b200 as M
+    return M
+
+
+def run(M, src, dst, t, V, motifs, delta):
+    g = M.Graph(src, dst, t, V, device=0)
+    tree = M.MGTree(motifs, delta)
+    out = M.comine(g, tree)
+    g.close()
+    tree.close()
+    return out
+
+
+def test_flat_fuzz(M, oracle_mod):
+    for seed in range(80):
+        rng = np.random.default_rng(3000 + seed)
+        V = int(rng.integers(3, 30))
+        src, dst, t, V = synth.random_graph(3000 + seed, V, int(rng.integers(1, 300)), int(rng.integers(5, 200)))
+        motifs = [synth.random_motif(seed * 13 + j, int(rng.integers(1, 5)), int(rng.integers(2, 6)))
+                  for j in range(int(rng.integers(1, 7)))]
+        delta = int(rng.integers(0, 80))
+        assert run(M, src, dst, t, V, motifs, delta) == oracle_mod.backtrack(src, dst, t, V, motifs, delta), seed
+
+
+def test_flat_hubs_and_c1(M, oracle_mod):
+    for seed in range(3):
+        src, dst, t, V = synth.random_graph(70 + seed, 5 + seed, 20_000, 4_000 + 3000 * seed, 0.01)
+        motifs = synth.group(synth.GROUP_C2) + [synth.MOTIFS["recip2"], synth.MOTIFS["repeat2"]]
+        assert run(M, src, dst, t, V, motifs, 10 + 7 * seed) == oracle_mod.backtrack(src, dst, t, V, motifs, 10 + 7 * seed)
+    cfg = synth.CONFIGS["C1"]
+    src, dst, t, V = cfg.graph()
+    assert run(M, src, dst, t, V, cfg.group(), cfg.delta) == oracle_mod.backtrack(src, dst, t, V, cfg.group(), cfg.delta)
+
+
+def test_flat_family_m3(M, oracle_mod):
+    from tests import _pins
+    fam = _pins.canonical_motifs(3)
+    assert len(fam) == 87
+    src, dst, t, V = synth.random_graph(17, 12, 1500, 400, 0.02)
+    assert run(M, src, dst, t, V, fam, 40) == oracle_mod.backtrack(src, dst, t, V, fam, 40)
+
+
+def test_flat_overflow_fallbacks(M, oracle_mod, monkeypatch):
+    monkeypatch.setenv("MAYURA_FLAT_WIN_CAP", "7")
+    monkeypatch.setenv("MAYURA_BFS_SEG_CAP", "3")
+    cfg = synth.CONFIGS["C1"]
+    src, dst, t, V = cfg.graph()
+    motifs = synth.group(synth.GROUP_C2) + [[(0, 1), (2, 3), (3, 0)]]
+    assert run(M, src, dst, t, V, motifs, cfg.delta) == oracle_mod.backtrack(src, dst, t, V, motifs, cfg.delta)

@@ -260,6 +260,10 @@ uint32_t hybrid_levels() {
 
 // ---- BFS passes (v4): per level an expand pass and a long-window pass
 constexpr uint32_t kCtlWords = bfs::kStripes + 2;  // per level: stripe counters, long counter, pad
+// control words: per level kCtlWords | 16 misc (fallback count, light-root count) | flat form:
+// per level kStripes window-piece stripe counters
+constexpr uint32_t kCtlFlat = kCtlWords * bfs::kMaxLevels + 16;
+constexpr uint32_t kCtlTotal = kCtlFlat + bfs::kStripes * bfs::kMaxLevels;
 
 template <int MAXV, bool L0, bool STATS>
 cudaError_t launch_bfs_pass(const bfs::BParams &p, bool long_pass, cudaStream_t s, int sms) {
@@ -379,7 +383,7 @@ mayura_status ensure_bfs_buffers(mayura_graph_s *g, uint32_t words, int nbufs) {
     }
     g->bfs_seg_cap = std::min(seg_cap, (uint32_t)(g->bfs_bytes / ((size_t)bfs::kStripes * rec_bytes)));
     if (!g->d_bfs_ctl) {
-        CK((cudaError_t)dmalloc((void **)&g->d_bfs_ctl, sizeof(uint32_t) * (kCtlWords * bfs::kMaxLevels + 16)),
+        CK((cudaError_t)dmalloc((void **)&g->d_bfs_ctl, sizeof(uint32_t) * kCtlTotal),
            "cudaMalloc(bfs ctl)");
         g->fresh_alloc = true;
         g->bfs_long_cap = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(g->E, 1u << 20), 1u << 28);
@@ -406,9 +410,8 @@ cudaError_t launch_flat_v(bfs::BParams p, uint32_t levels, uint32_t *bufs[2], ui
         flat::FParams f;
         f.b = p;
         f.win = win;
-        f.win_cnt = ctl + L * kCtlWords + bfs::kStripes;
-        f.cursor = ctl + L * kCtlWords + bfs::kStripes + 1;
-        f.win_cap = win_cap;
+        f.win_cnt = ctl + kCtlFlat + L * bfs::kStripes;
+        f.win_seg_cap = win_cap / bfs::kStripes;
         cudaError_t e = L == 0 ? launch_flat_level<MAXV, true>(f, s, sms) : launch_flat_level<MAXV, false>(f, s, sms);
         if (e != cudaSuccess) return e;
     }
@@ -597,7 +600,7 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         bs = ensure_flat_win(g);
         if (bs != MAYURA_OK) return bs;
         uint32_t *ctl = g->d_bfs_ctl;
-        CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * (kCtlWords * bfs::kMaxLevels + 16), s), "cudaMemsetAsync(ctl)");
+        CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * kCtlTotal, s), "cudaMemsetAsync(ctl)");
         bfs::BParams b = bfs_params(g, dt, r0, n_roots, counts, nullptr, 0u);
         uint32_t *bufs[2] = {g->d_bfs[0], g->d_bfs[1]};
         CK(launch_flat(b, dt.max_vertices, fl, bufs, ctl, g->bfs_seg_cap, reinterpret_cast<uint4 *>(g->d_flat_win),
@@ -611,7 +614,7 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         mayura_status bs = ensure_bfs_buffers(g, words, levels >= 2 ? 2 : 1);
         if (bs != MAYURA_OK) return bs;
         uint32_t *ctl = g->d_bfs_ctl;
-        CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * (kCtlWords * bfs::kMaxLevels + 16), s), "cudaMemsetAsync(ctl)");
+        CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * kCtlTotal, s), "cudaMemsetAsync(ctl)");
         bfs::BParams b = bfs_params(g, dt, r0, n_roots, counts, stats, kind == K_BFS ? 1u : 0u);
         if (kind == K_HYBRID && levels == 1) b.heavy_min = heavy_min(g);
         if (b.heavy_min) b.light = g->d_light;  // light roots are listed for the depth-first kernel

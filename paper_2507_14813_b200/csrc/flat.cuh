@@ -25,11 +25,12 @@ constexpr int kTB = 256;
 constexpr uint32_t kPiece = 64;  // entries per window piece (bounds one warp-round batch)
 
 struct FParams {
-    bfs::BParams b;      // graph, table, frontier in (F_k) / out (F_{k+1}), counts
-    uint4 *win;          // window pieces {x, group, start, n}; x = root edge id (k = 0) or F_k index
-    uint32_t *win_cnt;   // [0] pieces appended at this level (may exceed win_cap)
-    uint32_t *cursor;    // [0] pieces taken by the entry pass
-    uint32_t win_cap;
+    bfs::BParams b;        // graph, table, frontier in (F_k) / out (F_{k+1}), counts
+    uint4 *win;            // window pieces {x, group, start, n}; x = root edge id (k = 0) or F_k index;
+                           // kStripes segments of win_seg_cap pieces (a warp appends to stripe
+                           // warp mod kStripes: one hot counter would serialise every append)
+    uint32_t *win_cnt;     // kStripes counters: pieces appended (may exceed win_seg_cap)
+    uint32_t win_seg_cap;
 };
 
 // first position q in [lo, sent] with ent[q].x > key; ent[sent] is the list's sentinel (> any
@@ -119,15 +120,17 @@ __global__ void __launch_bounds__(kTB) flat_win_kernel(const __grid_constant__ F
             }
             const uint32_t total = __shfl_sync(kFull, incl, 31);
             uint32_t wb = 0;
-            if (lane_id == 0 && total) wb = atomicAdd(f.win_cnt, total);
+            const uint32_t seg = bfs::out_seg();
+            if (lane_id == 0 && total) wb = atomicAdd(f.win_cnt + seg, total);
             wb = __shfl_sync(kFull, wb, 0);
             const uint32_t at = wb + incl - np;
+            uint4 *wseg = f.win + (size_t)seg * f.win_seg_cap;
             if (np) {
-                if (at + np <= f.win_cap) {
+                if (at + np <= f.win_seg_cap) {
                     for (uint32_t q = 0; q < np; q++)
-                        f.win[at + q] = make_uint4(xid, g, lo + q * kPiece, min(kPiece, n - q * kPiece));
+                        wseg[at + q] = make_uint4(xid, g, lo + q * kPiece, min(kPiece, n - q * kPiece));
                 } else {  // no room: empty the reserved slots that exist, mine the rest in place
-                    for (uint32_t q = at; q < at + np && q < f.win_cap; q++) f.win[q] = make_uint4(0, 0, 0, 0);
+                    for (uint32_t q = at; q < at + np && q < f.win_seg_cap; q++) wseg[q] = make_uint4(0, 0, 0, 0);
                     atomicAdd(p.fallback, 1u);
                     bfs::dfs<MAXV, false>(p, s.nodes, s.groups, x, c, g);
                     fell = true;
@@ -151,14 +154,32 @@ __global__ void __launch_bounds__(kTB) flat_entry_kernel(const __grid_constant__
     for (int i = 0; i < ST_N; i++) c.st[i] = 0;
     c.em_next = c.em_end = 0;
     const uint32_t lane_id = threadIdx.x & 31;
-    const uint32_t n_win = min(*(volatile uint32_t *)f.win_cnt, f.win_cap);
-    for (;;) {
-        uint32_t wb = 0;
-        if (lane_id == 0) wb = atomicAdd(f.cursor, 32u);
-        wb = __shfl_sync(kFull, wb, 0);
-        if (wb >= n_win) break;
+    __shared__ uint32_t s_wpre[bfs::kStripes + 1];  // prefix of the pieces per stripe
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (int i = 0; i < bfs::kStripes; i++) {
+            s_wpre[i] = acc;
+            acc += min(f.win_cnt[i], f.win_seg_cap);
+        }
+        s_wpre[bfs::kStripes] = acc;
+    }
+    __syncthreads();
+    const uint32_t n_win = s_wpre[bfs::kStripes];
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, n_warps = (gridDim.x * blockDim.x) >> 5;
+    // pieces are <= kPiece entries, so a static interleaved batch assignment balances well and
+    // needs no shared cursor
+    for (uint32_t wb = gw * 32u; wb < n_win; wb += n_warps * 32u) {
         const uint32_t wi = wb + lane_id;
-        const uint4 w = wi < n_win ? f.win[wi] : make_uint4(0, 0, 0, 0);
+        uint4 w = make_uint4(0, 0, 0, 0);
+        if (wi < n_win) {
+            int lo = 0, hi = bfs::kStripes - 1;  // stripe s with s_wpre[s] <= wi < s_wpre[s + 1]
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_wpre[mid] <= wi) lo = mid;
+                else hi = mid - 1;
+            }
+            w = f.win[(size_t)lo * f.win_seg_cap + (wi - s_wpre[lo])];
+        }
         const uint32_t n = w.w;
         bfs::PM<MAXV> x;
         x.node = 0; x.nv = 0; x.root = 0; x.h = 0;

@@ -336,7 +336,7 @@ cudaError_t launch_flat_level(const flat::FParams &f, cudaStream_t s, int sms) {
 
 template <int MAXV>
 cudaError_t launch_flat_v(bfs::BParams p, uint32_t levels, uint32_t *bufs[2], uint32_t *ctl, uint32_t seg_cap,
-                          uint4 *win, uint32_t win_cap, cudaStream_t s, int sms);
+                          uint4 *win, uint32_t win_cap, const uint32_t *gwant, cudaStream_t s, int sms);
 
 uint32_t rec_words(uint32_t max_vertices) {
     const uint32_t mv = max_vertices <= 4 ? 4 : max_vertices <= 6 ? 6 : max_vertices <= 8 ? 8 : 16;
@@ -399,7 +399,7 @@ mayura_status ensure_bfs_buffers(mayura_graph_s *g, uint32_t words, int nbufs) {
 
 template <int MAXV>
 cudaError_t launch_flat_v(bfs::BParams p, uint32_t levels, uint32_t *bufs[2], uint32_t *ctl, uint32_t seg_cap,
-                          uint4 *win, uint32_t win_cap, cudaStream_t s, int sms) {
+                          uint4 *win, uint32_t win_cap, const uint32_t *gwant, cudaStream_t s, int sms) {
     for (uint32_t L = 0; L < levels; L++) {
         p.in.data = L ? bufs[(L - 1) & 1] : nullptr;
         p.in.cnt = L ? ctl + (L - 1) * kCtlWords : nullptr;
@@ -412,6 +412,7 @@ cudaError_t launch_flat_v(bfs::BParams p, uint32_t levels, uint32_t *bufs[2], ui
         f.win = win;
         f.win_cnt = ctl + kCtlFlat + L * bfs::kStripes;
         f.win_seg_cap = win_cap / bfs::kStripes;
+        f.gwant = gwant;
         cudaError_t e = L == 0 ? launch_flat_level<MAXV, true>(f, s, sms) : launch_flat_level<MAXV, false>(f, s, sms);
         if (e != cudaSuccess) return e;
     }
@@ -419,26 +420,34 @@ cudaError_t launch_flat_v(bfs::BParams p, uint32_t levels, uint32_t *bufs[2], ui
 }
 
 cudaError_t launch_flat(const bfs::BParams &p, uint32_t max_vertices, uint32_t levels, uint32_t *bufs[2], uint32_t *ctl,
-                        uint32_t seg_cap, uint4 *win, uint32_t win_cap, cudaStream_t s, int sms) {
-    if (max_vertices <= 4) return launch_flat_v<4>(p, levels, bufs, ctl, seg_cap, win, win_cap, s, sms);
-    if (max_vertices <= 6) return launch_flat_v<6>(p, levels, bufs, ctl, seg_cap, win, win_cap, s, sms);
-    if (max_vertices <= 8) return launch_flat_v<8>(p, levels, bufs, ctl, seg_cap, win, win_cap, s, sms);
-    return launch_flat_v<16>(p, levels, bufs, ctl, seg_cap, win, win_cap, s, sms);
+                        uint32_t seg_cap, uint4 *win, uint32_t win_cap, const uint32_t *gwant, cudaStream_t s, int sms) {
+    if (max_vertices <= 4) return launch_flat_v<4>(p, levels, bufs, ctl, seg_cap, win, win_cap, gwant, s, sms);
+    if (max_vertices <= 6) return launch_flat_v<6>(p, levels, bufs, ctl, seg_cap, win, win_cap, gwant, s, sms);
+    if (max_vertices <= 8) return launch_flat_v<8>(p, levels, bufs, ctl, seg_cap, win, win_cap, gwant, s, sms);
+    return launch_flat_v<16>(p, levels, bufs, ctl, seg_cap, win, win_cap, gwant, s, sms);
 }
 
-// Window-piece buffer of the flat form: 8 pieces per edge, >= 2^20, <= 15 % of free memory.
+// Window-piece buffer of the flat form: bytes for 8 pieces of 48 B per edge, >= 48 MiB, <= 15 %
+// of the free memory; its capacity in pieces depends on the tree's piece size.
+uint32_t piece_bytes(uint32_t max_vertices) {
+    const uint32_t mv = max_vertices <= 4 ? 4 : max_vertices <= 6 ? 6 : max_vertices <= 8 ? 8 : 16;
+    return 4 * ((6 + mv + 3) & ~3u);
+}
 mayura_status ensure_flat_win(mayura_graph_s *g) {
     if (g->d_flat_win) return MAYURA_OK;
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    uint64_t cap = std::max<uint64_t>(1u << 20, std::min<uint64_t>(8 * g->E, (uint64_t)(free_b * 0.15) / 16));
-    cap = std::min<uint64_t>(cap, 0xFFFFFFFFull);
-    if (const char *e = getenv("MAYURA_FLAT_WIN_CAP")) cap = (uint64_t)std::max(1L, atol(e));  // test hook
-    CK((cudaError_t)dmalloc((void **)&g->d_flat_win, 16 * cap), "cudaMalloc(window pieces)");
-    g->flat_win_cap = (uint32_t)cap;
-    g->device_bytes += 16 * cap;
+    const uint64_t bytes = std::max<uint64_t>(48ull << 20, std::min<uint64_t>(8 * 48 * g->E, (uint64_t)(free_b * 0.15)));
+    CK((cudaError_t)dmalloc((void **)&g->d_flat_win, bytes), "cudaMalloc(window pieces)");
+    g->flat_win_bytes = bytes;
+    g->device_bytes += bytes;
     g->fresh_alloc = true;
     return MAYURA_OK;
+}
+uint32_t flat_win_cap(const mayura_graph_s *g, uint32_t max_vertices) {
+    uint64_t cap = std::min<uint64_t>(g->flat_win_bytes / piece_bytes(max_vertices), 0xFFFFFFFFull);
+    if (const char *e = getenv("MAYURA_FLAT_WIN_CAP")) cap = std::min<uint64_t>(cap, (uint64_t)std::max(1L, atol(e)));
+    return (uint32_t)cap;  // (MAYURA_FLAT_WIN_CAP: test hook forcing the depth-first fallback)
 }
 
 void table_view(const Table &t, uint32_t n_motifs, char *buf, DeviceTable &d) {
@@ -604,7 +613,7 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         bfs::BParams b = bfs_params(g, dt, r0, n_roots, counts, nullptr, 0u);
         uint32_t *bufs[2] = {g->d_bfs[0], g->d_bfs[1]};
         CK(launch_flat(b, dt.max_vertices, fl, bufs, ctl, g->bfs_seg_cap, reinterpret_cast<uint4 *>(g->d_flat_win),
-                       g->flat_win_cap, s, sms),
+                       flat_win_cap(g, dt.max_vertices), dt.gwant, s, sms),
            "flat pass launch");
         return MAYURA_OK;
     }

@@ -26,11 +26,20 @@ constexpr uint32_t kPiece = 64;  // entries per window piece (bounds one warp-ro
 
 struct FParams {
     bfs::BParams b;        // graph, table, frontier in (F_k) / out (F_{k+1}), counts
-    uint4 *win;            // window pieces {x, group, start, n}; x = root edge id (k = 0) or F_k index;
-                           // kStripes segments of win_seg_cap pieces (a warp appends to stripe
-                           // warp mod kStripes: one hot counter would serialise every append)
+    uint4 *win;            // window pieces (Piece<MAXV>); kStripes segments of win_seg_cap pieces (a
+                           // warp appends to stripe warp mod kStripes: one hot counter would
+                           // serialise every append)
     uint32_t *win_cnt;     // kStripes counters: pieces appended (may exceed win_seg_cap)
     uint32_t win_seg_cap;
+    const uint32_t *gwant; // per group: wants of its first 4 children (bytes, 0xFD pad)
+};
+
+// A window piece carries everything the entry pass needs about its partial match, so the
+// entry pass loads nothing but the piece and the window entries:
+//   words [root, group | nv << 16, start, n, node, h, m2g[0..MAXV-1]], padded to uint4s
+template <int MAXV>
+struct Piece {
+    static constexpr int W = (6 + MAXV + 3) & ~3;
 };
 
 // first position q in [lo, sent] with ent[q].x > key; ent[sent] is the list's sentinel (> any
@@ -124,13 +133,25 @@ __global__ void __launch_bounds__(kTB) flat_win_kernel(const __grid_constant__ F
             if (lane_id == 0 && total) wb = atomicAdd(f.win_cnt + seg, total);
             wb = __shfl_sync(kFull, wb, 0);
             const uint32_t at = wb + incl - np;
-            uint4 *wseg = f.win + (size_t)seg * f.win_seg_cap;
+            constexpr int PW = Piece<MAXV>::W / 4;  // uint4s per piece
+            uint4 *wseg = f.win + (size_t)seg * f.win_seg_cap * PW;
             if (np) {
                 if (at + np <= f.win_seg_cap) {
-                    for (uint32_t q = 0; q < np; q++)
-                        wseg[at + q] = make_uint4(xid, g, lo + q * kPiece, min(kPiece, n - q * kPiece));
+                    for (uint32_t q = 0; q < np; q++) {
+                        uint4 *pc = wseg + (size_t)(at + q) * PW;
+                        pc[0] = make_uint4(x.root, g | (x.nv << 16), lo + q * kPiece, min(kPiece, n - q * kPiece));
+                        uint32_t w[PW * 4 - 4];
+                        w[0] = x.node;
+                        w[1] = x.h;
+#pragma unroll
+                        for (int k = 0; k < MAXV; k++) w[2 + k] = x.m2g[k];
+#pragma unroll
+                        for (int k = 2 + MAXV; k < PW * 4 - 4; k++) w[k] = 0;
+#pragma unroll
+                        for (int k = 1; k < PW; k++) pc[k] = make_uint4(w[4 * k - 4], w[4 * k - 3], w[4 * k - 2], w[4 * k - 1]);
+                    }
                 } else {  // no room: empty the reserved slots that exist, mine the rest in place
-                    for (uint32_t q = at; q < at + np && q < f.win_seg_cap; q++) wseg[q] = make_uint4(0, 0, 0, 0);
+                    for (uint32_t q = at; q < at + np && q < f.win_seg_cap; q++) wseg[(size_t)q * PW] = make_uint4(0, 0, 0, 0);
                     atomicAdd(p.fallback, 1u);
                     bfs::dfs<MAXV, false>(p, s.nodes, s.groups, x, c, g);
                     fell = true;
@@ -168,9 +189,14 @@ __global__ void __launch_bounds__(kTB) flat_entry_kernel(const __grid_constant__
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, n_warps = (gridDim.x * blockDim.x) >> 5;
     // pieces are <= kPiece entries, so a static interleaved batch assignment balances well and
     // needs no shared cursor
-    for (uint32_t wb = gw * 32u; wb < n_win; wb += n_warps * 32u) {
-        const uint32_t wi = wb + lane_id;
-        uint4 w = make_uint4(0, 0, 0, 0);
+    constexpr int PW = Piece<MAXV>::W / 4;
+    __shared__ uint32_t s_gw[lane::kGwMax];
+    for (uint32_t i = threadIdx.x; i < p.n_groups && i < lane::kGwMax; i += blockDim.x) s_gw[i] = f.gwant[i];
+    __syncthreads();
+    // piece wi of the level (global index over the stripes) -> registers (zeros past the end)
+    auto load_piece = [&](uint32_t wi, uint32_t (&pw)[PW * 4]) {
+#pragma unroll
+        for (int k = 0; k < PW * 4; k++) pw[k] = 0;
         if (wi < n_win) {
             int lo = 0, hi = bfs::kStripes - 1;  // stripe s with s_wpre[s] <= wi < s_wpre[s + 1]
             while (lo < hi) {
@@ -178,17 +204,26 @@ __global__ void __launch_bounds__(kTB) flat_entry_kernel(const __grid_constant__
                 if (s_wpre[mid] <= wi) lo = mid;
                 else hi = mid - 1;
             }
-            w = f.win[(size_t)lo * f.win_seg_cap + (wi - s_wpre[lo])];
+            const uint4 *pc = f.win + ((size_t)lo * f.win_seg_cap + (wi - s_wpre[lo])) * PW;
+#pragma unroll
+            for (int k = 0; k < PW; k++) {
+                const uint4 v = __ldcs(pc + k);  // streamed: read once
+                pw[4 * k] = v.x; pw[4 * k + 1] = v.y; pw[4 * k + 2] = v.z; pw[4 * k + 3] = v.w;
+            }
         }
+    };
+    for (uint32_t wb = gw * 32u; wb < n_win; wb += n_warps * 32u) {
+        uint32_t pw[PW * 4];
+        load_piece(wb + lane_id, pw);
+        const uint4 w = make_uint4(pw[0], pw[1], pw[2], pw[3]);
         const uint32_t n = w.w;
         bfs::PM<MAXV> x;
-        x.node = 0; x.nv = 0; x.root = 0; x.h = 0;
+        x.root = pw[0];
+        x.nv = pw[1] >> 16;
+        x.node = pw[4];
+        x.h = pw[5];
 #pragma unroll
-        for (int k = 0; k < MAXV; k++) x.m2g[k] = kNone;
-        if (n) {
-            if (L0) bfs::load_root<MAXV>(p, w.x, x);
-            else bfs::load_rec<MAXV>(p, s.pref, w.x, x);
-        }
+        for (int k = 0; k < MAXV; k++) x.m2g[k] = pw[6 + k];
         uint32_t incl = n;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -211,13 +246,19 @@ __global__ void __launch_bounds__(kTB) flat_entry_kernel(const __grid_constant__
             xo.nv = __shfl_sync(kFull, x.nv, o);
             xo.root = __shfl_sync(kFull, x.root, o);
             xo.h = __shfl_sync(kFull, x.h, o);
-            const uint32_t g = __shfl_sync(kFull, w.y, o);
+            const uint32_t g = __shfl_sync(kFull, w.y, o) & 0xffffu;
             const uint32_t pos = __shfl_sync(kFull, w.z, o) + (j - __shfl_sync(kFull, excl, o));
             uint32_t ch = kNone, etr = 0, e1 = 0, e2 = 0;
             DGroup G = s.groups[act ? g : 0];
             if (act) {
                 bfs::load_entry(p, G, pos, kNone, etr, e1, e2);
-                ch = bfs::find_child(s.nodes, G, bfs::entry_class<MAXV>(G, xo.m2g, e1, e2));
+                const uint32_t cls = bfs::entry_class<MAXV>(G, xo.m2g, e1, e2);
+                if (G.child_end - G.child_begin <= 4 && g < lane::kGwMax) {  // one SIMD byte compare
+                    const uint32_t eq = __vcmpeq4(s_gw[g], cls * 0x01010101u);
+                    ch = eq ? G.child_begin + ((__ffs(eq) - 1) >> 3) : kNone;
+                } else {
+                    ch = bfs::find_child(s.nodes, G, cls);
+                }
             }
             bool inner = false;
             if (ch != kNone) {

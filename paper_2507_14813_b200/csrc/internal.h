@@ -96,7 +96,7 @@ struct mayura_graph_s {
     uint32_t *d_bfs[2] = {nullptr, nullptr};             // BFS frontier buffers (ping-pong)
     uint32_t *d_bfs_ctl = nullptr, *d_bfs_long = nullptr;
     uint32_t *d_flat_win = nullptr;                      // flat form: window pieces (uint4)
-    uint32_t flat_win_cap = 0;
+    uint64_t flat_win_bytes = 0;
     uint32_t *d_light = nullptr;                         // hybrid: light roots listed by the BFS level (E + 32)
     size_t bfs_bytes = 0;
     int bfs_nbufs = 0;

@@ -224,13 +224,24 @@ cudaError_t launch_lane(const lane::LParams &p, uint32_t max_vertices, bool stat
     return launch_lane_v<16>(p, stats, generic, s, sms);
 }
 
-// Kernel choice (MAYURA_KERNEL): "hybrid" (default), "lane", "bfs", "flat".
+// Kernel form (MAYURA_KERNEL overrides): "flat" (level-synchronous, entry-parallel; flat.cuh),
+// "hybrid" (one breadth-first level + the depth-first lane kernel), "lane", "bfs".  Default:
+// flat when the graph arrays fit in L2, else hybrid.  Measured (profiles/README.md r04): flat
+// C1 0.172 -> 0.076 ms, C2 0.527 -> 0.321 ms; on DRAM-resident graphs its per-level frontier
+// and window-piece traffic loses (C3 4.9 ms hybrid vs 7.8 ms flat).
 enum KernelKind { K_HYBRID = 0, K_LANE = 1, K_BFS = 2, K_FLAT = 3 };
-KernelKind kernel_kind() {  // read per call (tests switch forms within one process)
+bool l2_resident(const mayura_graph_s *g) {
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
+    return g->graph_bytes <= (uint64_t)l2;
+}
+KernelKind kernel_kind(const mayura_graph_s *g) {  // read per call (tests switch forms within one process)
     const char *e = getenv("MAYURA_KERNEL");
-    return (e && std::strcmp(e, "lane") == 0) ? K_LANE
-           : (e && std::strcmp(e, "bfs") == 0) ? K_BFS
-           : (e && std::strcmp(e, "flat") == 0) ? K_FLAT : K_HYBRID;
+    if (e && std::strcmp(e, "lane") == 0) return K_LANE;
+    if (e && std::strcmp(e, "bfs") == 0) return K_BFS;
+    if (e && std::strcmp(e, "flat") == 0) return K_FLAT;
+    if (e && std::strcmp(e, "hybrid") == 0) return K_HYBRID;
+    return l2_resident(g) ? K_FLAT : K_HYBRID;
 }
 // hybrid: a root is split breadth-first only if one of its root-node windows has >= this
 // many entries; the breadth-first level lists the light ones for the depth-first kernel.
@@ -244,9 +255,7 @@ uint32_t heavy_min(const mayura_graph_s *g) {
         v = e ? std::max(0, atoi(e)) : -1;
     }
     if (v >= 0) return (uint32_t)v;
-    int l2 = 0;
-    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
-    return g->graph_bytes <= (uint64_t)l2 ? 8u : 16u;
+    return l2_resident(g) ? 8u : 16u;
 }
 // hybrid: breadth-first levels before the depth-first lane kernel (MAYURA_HYBRID_LEVELS)
 uint32_t hybrid_levels() {
@@ -597,7 +606,7 @@ bfs::BParams bfs_params(const mayura_graph_s *g, const DeviceTable &dt, uint32_t
 mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32_t n_roots, uint32_t *lb,
                    unsigned long long *counts, unsigned long long *stats, cudaStream_t s, int sms) {
     const bool st = stats != nullptr;
-    const KernelKind kind = kernel_kind();
+    const KernelKind kind = kernel_kind(g);
     const uint32_t words = rec_words(dt.max_vertices);
     uint32_t levels = 0;  // breadth-first levels before the depth-first phase
     if (kind == K_HYBRID) levels = std::min(hybrid_levels(), dt.max_edges > 2 ? dt.max_edges - 2 : 0u);
@@ -699,11 +708,12 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
         // allocation completes before the caller's stream uses it
         uint32_t mv = tabs[0].max_vertices;
         for (size_t i = 1; i < tabs.size(); i++) mv = std::max(mv, tabs[i].max_vertices);
-        if (kernel_kind() != K_LANE && n_roots > 0) {
-            const uint32_t lv = kernel_kind() == K_BFS || kernel_kind() == K_FLAT ? 2u : std::min(hybrid_levels(), 2u);
+        const KernelKind kind = kernel_kind(g);
+        if (kind != K_LANE && n_roots > 0) {
+            const uint32_t lv = kind == K_BFS || kind == K_FLAT ? 2u : std::min(hybrid_levels(), 2u);
             if (lv > 0) st = ensure_bfs_buffers(g, rec_words(mv), lv >= 2 ? 2 : 1);
             if (st != MAYURA_OK) return st;
-            if (kernel_kind() == K_FLAT) st = ensure_flat_win(g);
+            if (kind == K_FLAT) st = ensure_flat_win(g);
             if (st != MAYURA_OK) return st;
         }
         if (g->fresh_alloc) {

@@ -1,7 +1,9 @@
-"""GPU parity of the level-synchronous, entry-parallel kernel form (MAYURA_KERNEL=flat,
-csrc/flat.cuh) vs the oracle: random groups, hub lists, the C1 workload, the 87-motif
-3-edge family (every anchor kind incl. GLOBAL), and forced overflow of the window-piece
-and frontier buffers (the depth-first fallback must keep counts exact)."""
+"""GPU parity of each kernel form vs the oracle, forced with MAYURA_KERNEL: "flat" (level-
+synchronous, entry-parallel; csrc/flat.cuh; the default for graphs that fit in L2),
+"hybrid" (one breadth-first level + the depth-first lane kernel; the default for larger
+graphs) and "lane" (pure depth-first).  Random groups, hub lists, the C1 workload, the
+87-motif 3-edge family (every anchor kind incl. GLOBAL), and forced overflow of the
+window-piece and frontier buffers (the depth-first fallback must keep counts exact)."""
 import numpy as np
 import pytest
 
@@ -10,12 +12,12 @@ import synth
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture()
-def M(monkeypatch):
+@pytest.fixture(params=["flat", "hybrid", "lane"])
+def M(monkeypatch, request):
     import torch
     if not torch.cuda.is_available():
         pytest.fail("GPU tests need a CUDA device")
-    monkeypatch.setenv("MAYURA_KERNEL", "flat")
+    monkeypatch.setenv("MAYURA_KERNEL", request.param)
     import paper_2507_14813_b200 as M
     return M
 
@@ -29,7 +31,7 @@ def run(M, src, dst, t, V, motifs, delta):
     return out
 
 
-def test_flat_fuzz(M, oracle_mod):
+def test_form_fuzz(M, oracle_mod):
     for seed in range(80):
         rng = np.random.default_rng(3000 + seed)
         V = int(rng.integers(3, 30))
@@ -40,7 +42,7 @@ def test_flat_fuzz(M, oracle_mod):
         assert run(M, src, dst, t, V, motifs, delta) == oracle_mod.backtrack(src, dst, t, V, motifs, delta), seed
 
 
-def test_flat_hubs_and_c1(M, oracle_mod):
+def test_form_hubs_and_c1(M, oracle_mod):
     for seed in range(3):
         src, dst, t, V = synth.random_graph(70 + seed, 5 + seed, 20_000, 4_000 + 3000 * seed, 0.01)
         motifs = synth.group(synth.GROUP_C2) + [synth.MOTIFS["recip2"], synth.MOTIFS["repeat2"]]
@@ -50,7 +52,7 @@ def test_flat_hubs_and_c1(M, oracle_mod):
     assert run(M, src, dst, t, V, cfg.group(), cfg.delta) == oracle_mod.backtrack(src, dst, t, V, cfg.group(), cfg.delta)
 
 
-def test_flat_family_m3(M, oracle_mod):
+def test_form_family_m3(M, oracle_mod):
     from tests import _pins
     fam = _pins.canonical_motifs(3)
     assert len(fam) == 87
@@ -58,7 +60,7 @@ def test_flat_family_m3(M, oracle_mod):
     assert run(M, src, dst, t, V, fam, 40) == oracle_mod.backtrack(src, dst, t, V, fam, 40)
 
 
-def test_flat_overflow_fallbacks(M, oracle_mod, monkeypatch):
+def test_form_overflow_fallbacks(M, oracle_mod, monkeypatch):
     monkeypatch.setenv("MAYURA_FLAT_WIN_CAP", "7")
     monkeypatch.setenv("MAYURA_BFS_SEG_CAP", "3")
     cfg = synth.CONFIGS["C1"]

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_flat.py -x -q -p no:cacheprovider 2>&1 | tail -15
+timeout 600 python -m pytest tests/test_gpu_forms.py -x -q -p no:cacheprovider 2>&1 | tail -15
 for K in hybrid flat; do
  for C in C1 C2 C3; do
   MAYURA_KERNEL=$K timeout 300 python bench.py --config $C --no-cpu-baseline --no-e2e --no-indep --no-enum --steps 10 --warmup 3 > gpurun_out/fl_${K}_${C}.json 2>&1

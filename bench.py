@@ -31,6 +31,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+KERNELS = {"flat": "co-mining pass (flat form): per MG-Tree level flat::flat_win_kernel + flat::flat_entry_kernel",
+           "hybrid": "co-mining pass (hybrid form): bfs::expand_kernel + bfs::long_kernel + lane::comine_lane_kernel"}
 METRIC = "motif-group co-mining time (s) and root edges/s at 1/2/4/8 B200; HBM GB/s frac"
 UNIT = "root edges/s"
 
@@ -337,9 +339,10 @@ def main():
         tr = json.load(open(prof)).get(cfg.name)
         if tr:
             traffic = tr.get("dram_bytes_per_launch")
+    form = M.mayura_kernel_form(g.handle)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic,
-                "kernel": "co-mining pass: bfs::expand_kernel + bfs::long_kernel + lane::comine_lane_kernel",
+                "kernel": KERNELS.get(form, form), "kernel_form": form,
                 "kernel_ms": ms_kern,
                 "window_end_kernel_ms": ms_win, "bytes_alg_per_launch": st["bytes_alg"],
                 "bytes_alg_per_root": st["bytes_alg"] / max(1, re_ - rb), "peak_source": peak_src,
@@ -403,7 +406,7 @@ def main():
                "parity_vs_oracle": parity,
                "gpu_launches": launches * world,
                "gpu_launches_detail": "mayura_launch_count() over the timed steps x ranks: per step "
-                                      "window_end_kernel + expand_kernel + long_kernel + comine_lane_kernel",
+                                      "window_end_kernel + " + KERNELS.get(form, form),
                "roofline": roofline, "clocks": clocks, "e2e": e2e, "independent_gpu": indep,
                "cpu_baseline": cpu, "search_stats": st, "enumeration": enum}
         print(json.dumps(out), flush=True)

@@ -232,6 +232,13 @@ mayura_status mayura_comine_heuristic(mayura_graph g, mayura_mgtree m, int *use_
 mayura_status mayura_partition_roots(mayura_graph g, int64_t delta, uint32_t n_parts,
                                      uint64_t *bounds_out);
 
+/* Kernel form mayura_comine uses for this graph: "flat" (level-synchronous,
+ * entry-parallel; the default when the graph arrays fit in L2), "hybrid" (one breadth-first
+ * level + the depth-first lane kernel; the default otherwise), or "lane" / "bfs" when forced
+ * with the MAYURA_KERNEL environment variable; "none" for NULL or host-only graphs.  All
+ * forms return identical counts.  Static string. */
+const char *mayura_kernel_form(mayura_graph g);
+
 /* Thread-local message for the last failing call on this thread ("" if none). */
 const char *mayura_last_error(void);
 

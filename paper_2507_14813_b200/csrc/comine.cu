@@ -1007,3 +1007,13 @@ extern "C" mayura_status mayura_enumerate(mayura_graph g, mayura_mgtree m, uint6
     return run_enum(g, m, root_begin, root_end, cuda_stream, tuples_out, capacity_words, tuples_on_device,
                     counts_out, words_needed);
 }
+
+extern "C" const char *mayura_kernel_form(mayura_graph g) {
+    if (!g || g->device < 0) return "none";
+    switch (kernel_kind(g)) {
+        case K_FLAT: return "flat";
+        case K_LANE: return "lane";
+        case K_BFS: return "bfs";
+        default: return "hybrid";
+    }
+}

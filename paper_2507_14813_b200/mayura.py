@@ -48,6 +48,7 @@ SIGNATURES = {
     "mayura_enumerate": ([_P, _P, _u64, _u64, _P, _P, _u64, _int, _P, _P], _int),
     "mayura_comine_heuristic": ([_P, _P, _P, _P, _P], _int),
     "mayura_last_error": ([], ctypes.c_char_p),
+    "mayura_kernel_form": ([_P], ctypes.c_char_p),
     "mayura_version": ([], ctypes.c_char_p),
     "mayura_launch_count": ([], _u64),
 }
@@ -88,6 +89,10 @@ def mayura_last_error() -> str:
 
 def mayura_version() -> str:
     return _lib.mayura_version().decode()
+
+
+def mayura_kernel_form(g: int) -> str:
+    return _lib.mayura_kernel_form(g).decode()
 
 
 def mayura_launch_count() -> int:

@@ -187,3 +187,10 @@ def test_partition_roots(M):
         assert b == ref
         per = [int(proxy[a:c].sum()) for a, c in zip(b, b[1:])]
         assert max(per) <= sum(per) / parts + proxy.max()         # balanced up to one root
+
+
+def test_kernel_form_host_only_graph(M):
+    """mayura_kernel_form: 'none' for host-only graphs and NULL (no CUDA call is made)."""
+    g = M.Graph(np.array([0, 1], np.uint32), np.array([1, 2], np.uint32), np.array([1, 2], np.int64), 3, device=-1)
+    assert M.mayura_kernel_form(g.handle) == "none"
+    assert M.mayura_kernel_form(None) == "none"

@@ -479,6 +479,7 @@ __device__ __forceinline__ void flush(const BParams &p, const Smem &s, Ctx &c) {
 // ------------------------------------------------------------------ expand pass
 template <int MAXV, bool LEVEL0, bool STATS>
 __global__ void __launch_bounds__(kTB) expand_kernel(const __grid_constant__ BParams p) {
+    pdl_begin();
     extern __shared__ __align__(16) unsigned char smem[];
     const Smem s = smem_setup(p, smem, LEVEL0);
     Ctx c;
@@ -623,6 +624,7 @@ __global__ void __launch_bounds__(kTB) expand_kernel(const __grid_constant__ BPa
 // inner children handled by the lane that holds the matching entry.
 template <int MAXV, bool LEVEL0, bool STATS>
 __global__ void __launch_bounds__(kTB) long_kernel(const __grid_constant__ BParams p) {
+    pdl_begin();
     extern __shared__ __align__(16) unsigned char smem[];
     const Smem s = smem_setup(p, smem, LEVEL0);
     Ctx c;

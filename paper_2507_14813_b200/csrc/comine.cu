@@ -37,6 +37,15 @@ enum { ST_ROOTS, ST_NODES, ST_WINDOWS, ST_ENTRIES, ST_PROBES, ST_BATCHES, ST_BYT
 // per-launch scheduler words (zeroed by window_end_kernel): [LB_ROOT] = root / item cursor
 enum { LB_ROOT = 0, LB_N = 8 };
 
+// Programmatic dependent launch (sm_90+): every kernel of a query lets the next one be
+// scheduled at once (its blocks take SM slots as this grid's blocks retire, hiding launch
+// latency and the tail), then waits for the previous grid to complete and flush before it
+// touches anything -- so the dependency chain is unchanged.
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 #include "lane.cuh"
 #include "bfs.cuh"
 #include "flat.cuh"
@@ -47,6 +56,7 @@ enum { LB_ROOT = 0, LB_N = 8 };
 __global__ void window_end_kernel(const int64_t *__restrict__ T, uint32_t E, int64_t delta, uint32_t r0,
                                   uint32_t n_roots, uint32_t *__restrict__ hi, uint32_t *lb, uint32_t n_lb,
                                   unsigned long long *counts, uint32_t n_counts) {
+    pdl_begin();
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
     if (tid < n_lb) lb[tid] = 0;
     if (tid < n_counts) counts[tid] = 0;
@@ -72,6 +82,31 @@ __global__ void window_end_kernel(const int64_t *__restrict__ T, uint32_t E, int
         }
         hi[r] = a - 1;
     }
+}
+
+bool pdl_enabled() {  // MAYURA_PDL=0 launches without the attribute (A/B)
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("MAYURA_PDL");
+        v = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), uint32_t grid, uint32_t block, size_t smem, cudaStream_t s,
+                       Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 struct DeviceTable {
@@ -164,9 +199,9 @@ cudaError_t launch_lane_t(const lane::LParams &p, size_t smem, cudaStream_t s, i
         }
         grid = *grid_out;
     }
-    kern<<<grid, lane::kLB, smem, s>>>(p);
+    cudaError_t le = launch_pdl(kern, grid, lane::kLB, smem, s, p);
     count_launch();
-    return cudaGetLastError();
+    return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 constexpr size_t kLaneCntSmem = 48 * 1024;  // lane-private counters while they fit this budget
@@ -288,9 +323,9 @@ cudaError_t launch_bfs_pass(const bfs::BParams &p, bool long_pass, cudaStream_t 
         const uint32_t need = (p.n_roots + bfs::kTB - 1) / bfs::kTB;
         grid = std::max(1u, std::min(grid, need));
     }
-    kern<<<grid, bfs::kTB, smem, s>>>(p);
+    cudaError_t le = launch_pdl(kern, grid, bfs::kTB, smem, s, p);
     count_launch();
-    return cudaGetLastError();
+    return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 template <int MAXV>
@@ -335,9 +370,9 @@ cudaError_t launch_flat_level(const flat::FParams &f, cudaStream_t s, int sms) {
         if (e != cudaSuccess) return e;
         uint32_t grid = (uint32_t)(sms * (per_sm > 0 ? per_sm : 1));
         if (L0 && pass == 0) grid = std::max(1u, std::min(grid, (f.b.n_roots + flat::kTB - 1) / flat::kTB));
-        kern<<<grid, flat::kTB, smem, s>>>(f);
+        e = launch_pdl(kern, grid, flat::kTB, smem, s, f);
         count_launch();
-        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -729,9 +764,9 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
         blocks = std::max(blocks, minb);
         blocks = std::min<uint32_t>(blocks, 148u * 32u);
         if (blocks == 0) blocks = 1;
-        window_end_kernel<<<blocks, threads, 0, s>>>(g->d_t, (uint32_t)g->E, m->delta, (uint32_t)rb, n_roots,
-                                                     g->d_hi, g->d_queue, n_lb, d_counts, k);
-        CK(cudaGetLastError(), "window_end_kernel launch");
+        CK(launch_pdl(window_end_kernel, blocks, threads, 0, s, (const int64_t *)g->d_t, (uint32_t)g->E, m->delta,
+                      (uint32_t)rb, n_roots, g->d_hi, g->d_queue, n_lb, d_counts, k),
+           "window_end_kernel launch");
         count_launch();
     }
     if (mid_event) CK(cudaEventRecord((cudaEvent_t)mid_event, s), "cudaEventRecord(mid_event)");

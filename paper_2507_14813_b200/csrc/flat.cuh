@@ -83,6 +83,7 @@ __device__ __forceinline__ uint32_t window(const bfs::BParams &p, const DGroup &
 
 template <int MAXV, bool L0>
 __global__ void __launch_bounds__(kTB) flat_win_kernel(const __grid_constant__ FParams f) {
+    pdl_begin();
     extern __shared__ __align__(16) unsigned char smem[];
     const bfs::BParams &p = f.b;
     const bfs::Smem s = bfs::smem_setup(p, smem, L0);
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(kTB) flat_win_kernel(const __grid_constant__ F
 
 template <int MAXV, bool L0>
 __global__ void __launch_bounds__(kTB) flat_entry_kernel(const __grid_constant__ FParams f) {
+    pdl_begin();
     extern __shared__ __align__(16) unsigned char smem[];
     const bfs::BParams &p = f.b;
     const bfs::Smem s = bfs::smem_setup(p, smem, L0);

@@ -187,6 +187,7 @@ __device__ __forceinline__ uint32_t pick4(const uint4 &v, uint32_t k) {
 template <int MAXV, bool LANECNT, bool STATS, bool GEN, bool ENUM = false>
 __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_constant__ LParams p) {
     constexpr int FW = frame_words(ENUM);
+    pdl_begin();
     constexpr int TW = task_words(MAXV, ENUM);
     extern __shared__ __align__(16) unsigned char smem[];
     LNode *s_nodes = reinterpret_cast<LNode *>(smem);

@@ -696,6 +696,7 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
     if (!counts_out && !stats_host) return fail(MAYURA_E_INVALID, "mayura_comine: counts_out is NULL");
     DeviceGuard guard(g->device);
     cudaStream_t s = (cudaStream_t)stream;
+    trace("comine: enter");
     std::vector<DeviceTable> tabs;
     mayura_status st = ensure_tables(m, g->device, tabs);
     if (st != MAYURA_OK) return st;
@@ -756,6 +757,7 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
             g->fresh_alloc = false;
         }
     }
+    trace("comine: tables + scratch");
     const uint32_t n_lb = (uint32_t)(LB_N * n_launch);
     {
         const int threads = 256;
@@ -779,6 +781,7 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
             if (st != MAYURA_OK) return st;
         }
     }
+    trace("comine: kernels");
     if (stats_host) {
         CK(cudaMemcpyAsync(stats_host, g->d_stats, sizeof(unsigned long long) * ST_N, cudaMemcpyDeviceToHost, s),
            "cudaMemcpyAsync(stats)");
@@ -789,6 +792,7 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
     }
     if (!on_device || stats_host) {
         CK(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        trace("comine: D2H + sync");
         if (dbg_path && g->d_dbg) {
             std::vector<unsigned long long> rec(8 * kDbgWarps);
             CK(cudaMemcpy(rec.data(), g->d_dbg, rec.size() * 8, cudaMemcpyDeviceToHost), "cudaMemcpy(dbg)");
@@ -935,18 +939,91 @@ mayura_status run_enum(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint6
     return rs;
 }
 
+// Per-device cache of one graph's query scratch (frontier, window pieces, control words,
+// long-window items, light-root list, queue words), handed to the next graph loaded on the
+// device: the e2e path builds and drops a graph per query, and sizing + allocating the
+// scratch cost ~0.2 ms per new graph (MAYURA_TRACE, C2).  A graph owns its scratch while it
+// lives, so distinct handles stay independent.
+struct ScratchSet {
+    bool valid = false;
+    uint64_t e_cap = 0;  // scratch was sized for graphs of up to this many edges
+    uint32_t *bfs[2] = {nullptr, nullptr};
+    size_t bfs_bytes = 0;
+    int bfs_nbufs = 0;
+    uint32_t bfs_words = 0, bfs_seg_cap = 0, bfs_long_cap = 0;
+    uint32_t *ctl = nullptr, *lng = nullptr, *light = nullptr, *flat_win = nullptr, *queue = nullptr;
+    uint64_t flat_win_bytes = 0, bytes = 0;
+};
+std::mutex g_scratch_mu;
+ScratchSet g_scratch[64];
+
+void free_scratch_set(ScratchSet &c) {
+    void *ptrs[] = {c.bfs[0], c.bfs[1], c.ctl, c.lng, c.light, c.flat_win, c.queue};
+    for (void *p : ptrs) dfree(p);
+    c = ScratchSet();
+}
+
+// called with the graph's device current: keep g's scratch for the next graph, else free it
+void stash_scratch(mayura_graph_s *g) {
+    if (g->device < 0 || g->device >= 64) return;
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    ScratchSet &c = g_scratch[g->device];
+    if (!g->d_bfs_ctl || !g->d_light || !g->d_queue) return;  // nothing reusable (freed with the graph)
+    if (c.valid) free_scratch_set(c);
+    c.valid = true;
+    c.e_cap = g->E;
+    c.bfs[0] = g->d_bfs[0]; c.bfs[1] = g->d_bfs[1];
+    c.bfs_bytes = g->bfs_bytes; c.bfs_nbufs = g->bfs_nbufs; c.bfs_words = g->bfs_words;
+    c.bfs_seg_cap = g->bfs_seg_cap; c.bfs_long_cap = g->bfs_long_cap;
+    c.ctl = g->d_bfs_ctl; c.lng = g->d_bfs_long; c.light = g->d_light;
+    c.flat_win = g->d_flat_win; c.flat_win_bytes = g->flat_win_bytes;
+    c.queue = g->d_queue;
+    g->d_bfs[0] = g->d_bfs[1] = nullptr;
+    g->d_bfs_ctl = g->d_bfs_long = g->d_light = g->d_flat_win = g->d_queue = nullptr;
+}
+
+// before building a graph of E edges on `device`: drop a cached set too small for it (so its
+// memory is available to the build)
+void drop_small_scratch(int device, uint64_t E) {
+    if (device < 0 || device >= 64) return;
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    ScratchSet &c = g_scratch[device];
+    if (c.valid && c.e_cap < E) {
+        cudaDeviceSynchronize();
+        free_scratch_set(c);
+    }
+}
+
+// after building g: adopt the cached set if it was sized for at least g->E edges
+void adopt_scratch(mayura_graph_s *g) {
+    if (g->device < 0 || g->device >= 64) return;
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    ScratchSet &c = g_scratch[g->device];
+    if (!c.valid || c.e_cap < g->E) return;
+    if (getenv("MAYURA_BFS_LONG_CAP")) return;  // test hook sizing: allocate afresh
+    g->d_bfs[0] = c.bfs[0]; g->d_bfs[1] = c.bfs[1];
+    g->bfs_bytes = c.bfs_bytes; g->bfs_nbufs = c.bfs_nbufs; g->bfs_words = c.bfs_words;
+    g->bfs_seg_cap = c.bfs_seg_cap; g->bfs_long_cap = c.bfs_long_cap;
+    g->d_bfs_ctl = c.ctl; g->d_bfs_long = c.lng; g->d_light = c.light;
+    g->d_flat_win = c.flat_win; g->flat_win_bytes = c.flat_win_bytes;
+    g->d_queue = c.queue;
+    g->device_bytes += (uint64_t)c.bfs_nbufs * c.bfs_bytes + c.flat_win_bytes + 4ull * 3 * c.bfs_long_cap +
+                       4ull * (c.e_cap + 32);
+    c = ScratchSet();
+}
+
 void free_device(mayura_graph_s *g) {
     if (g->device < 0) return;
     DeviceGuard guard(g->device);
+    cudaDeviceSynchronize();  // no queued work may still use the memory returned to the pool
+    stash_scratch(g);
     void *ptrs[] = {g->d_src, g->d_dst, g->d_tr, g->d_hi, g->d_t, g->d_out_off, g->d_in_off, g->d_out_ent,
                     g->d_in_ent, g->d_eptr, g->d_out_ptr, g->d_in_ptr, g->d_perm, g->d_queue, g->d_counts,
                     g->d_stats, g->d_dbg, g->d_bfs[0], g->d_bfs[1], g->d_bfs_ctl, g->d_bfs_long, g->d_light,
                     g->d_out_rank, g->d_in_rank, g->d_enum, g->d_flat_win};
-    cudaDeviceSynchronize();  // no queued work may still use the memory returned to the pool
     for (void *p : ptrs) dfree(p);
     cudaStreamSynchronize(0);
 }
-
 }  // namespace
 
 void free_mgtree_device(mayura_mgtree_s *m) { free_tables(m); }
@@ -989,7 +1066,9 @@ extern "C" mayura_status mayura_load_graph(const uint32_t *src, const uint32_t *
     g->device = device;
     {
         DeviceGuard guard(device);
+        drop_small_scratch(device, n_edges);
         s = build_graph_device(src, dst, t, n_edges, n_vertices, g);  // step a0 on the GPU (graph_gpu.cu)
+        if (s == MAYURA_OK) adopt_scratch(g);
     }
     if (s != MAYURA_OK) {
         free_device(g);

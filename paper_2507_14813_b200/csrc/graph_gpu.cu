@@ -21,6 +21,9 @@
 #include <cub/device/device_scan.cuh>
 
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <type_traits>
@@ -226,6 +229,17 @@ static std::atomic<uint64_t> g_launches{0};
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+void trace(const char *what) {
+    static int on = -1;
+    if (on < 0) on = getenv("MAYURA_TRACE") ? 1 : 0;
+    if (!on) return;
+    static auto last = std::chrono::steady_clock::now();
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[mayura] %-28s %9.1f us\n", what, std::chrono::duration<double, std::micro>(now - last).count());
+    last = std::chrono::steady_clock::now();
+}
+
 int dmalloc(void **p, size_t bytes) {
     static std::mutex mu;
     static bool pooled[64] = {};
@@ -255,6 +269,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
         return fail(MAYURA_E_LIMIT, "mayura_load_graph: n_edges + n_vertices exceeds 32-bit list positions");
     const uint32_t E = (uint32_t)E64;
     const size_t N = (size_t)E + V;  // list positions incl. sentinels
+    trace("load: enter");
     g->E = E;
     g->V = V;
     g->host_built = false;
@@ -296,6 +311,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     GK(tmp.get(idst, E), "cudaMalloc(tmp)");
     GK(tmp.get(it, E), "cudaMalloc(tmp)");
     GK(tmp.get(bad, 4), "cudaMalloc(tmp)");
+    trace("load: allocations");
     GK(cudaMemcpyAsync(isrc, hsrc, 4ull * E, cudaMemcpyHostToDevice, s), "H2D(src)");
     GK(cudaMemcpyAsync(idst, hdst, 4ull * E, cudaMemcpyHostToDevice, s), "H2D(dst)");
     GK(cudaMemcpyAsync(it, ht, 8ull * E, cudaMemcpyHostToDevice, s), "H2D(t)");
@@ -326,6 +342,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
         tmin = hm[0];
         tmax = hm[1];
     }
+    trace("load: H2D + id check + minmax");
     // 1. stable sort by (t, input rank)
     GK(tmp.get(key, E), "cudaMalloc(tmp)");
     GK(tmp.get(key2, E), "cudaMalloc(tmp)");
@@ -342,6 +359,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
         // 2. time ranks
         k_time_rank<<<blocks_for(E), kT, 0, s>>>(g->d_t, g->d_tr, E); count_launch();
     }
+    trace("load: time sort + ranks");
     // 3. out / in adjacency
     GK(tmp.get(skey, E), "cudaMalloc(tmp)");
     GK(tmp.get(val2, E), "cudaMalloc(tmp)");
@@ -365,6 +383,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
         }
         k_offsets<<<blocks_for((uint64_t)V + 1), kT, 0, s>>>(skey, E, V, off); count_launch();
     }
+    trace("load: out/in CSR");
     // 4. successor pointers, then each list entry's copy of them
     if (E) {
         k_succ<<<blocks_for(E), kT, 0, s>>>(g->d_src, g->d_dst, g->d_tr, g->d_out_off,
@@ -383,6 +402,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     }
     GK(cudaGetLastError(), "graph build kernels");
     GK(cudaStreamSynchronize(s), "graph build");
+    trace("load: successor pointers");
     return MAYURA_OK;
 }
 

@@ -146,6 +146,9 @@ mayura_status build_graph_host(const uint32_t *src, const uint32_t *dst, const i
 mayura_status compile_tree(const uint32_t *motif_edges, const uint32_t *motif_len,
                            uint32_t n_motifs, int64_t delta, mayura_mgtree_s *m);
 int host_threads();
+// MAYURA_TRACE=1: synchronise the device and print the host time since the previous trace
+// point (diagnostic of the e2e path; perturbs timing, never on by default)
+void trace(const char *what);
 }  // namespace mayura
 
 namespace mayura {

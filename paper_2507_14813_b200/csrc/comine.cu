@@ -1017,10 +1017,8 @@ void free_device(mayura_graph_s *g) {
     DeviceGuard guard(g->device);
     cudaDeviceSynchronize();  // no queued work may still use the memory returned to the pool
     stash_scratch(g);
-    void *ptrs[] = {g->d_src, g->d_dst, g->d_tr, g->d_hi, g->d_t, g->d_out_off, g->d_in_off, g->d_out_ent,
-                    g->d_in_ent, g->d_eptr, g->d_out_ptr, g->d_in_ptr, g->d_perm, g->d_queue, g->d_counts,
-                    g->d_stats, g->d_dbg, g->d_bfs[0], g->d_bfs[1], g->d_bfs_ctl, g->d_bfs_long, g->d_light,
-                    g->d_out_rank, g->d_in_rank, g->d_enum, g->d_flat_win};
+    void *ptrs[] = {g->d_arena, g->d_queue, g->d_counts, g->d_stats, g->d_dbg, g->d_bfs[0], g->d_bfs[1],
+                    g->d_bfs_ctl, g->d_bfs_long, g->d_light, g->d_enum, g->d_flat_win};  // arena: graph arrays
     for (void *p : ptrs) dfree(p);
     cudaStreamSynchronize(0);
 }

@@ -275,32 +275,52 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     g->host_built = false;
     cudaStream_t s = nullptr;
     uint64_t bytes = 0;
+    // all product arrays live in ONE allocation (the e2e path builds a graph per query; one
+    // pool allocation instead of 15): a planning pass sums the 256-byte-aligned sizes, a
+    // second pass carves the arena and fills
+    char *arena = nullptr;
+    size_t off = 0;
+    bool plan = true;
     auto alloc = [&](auto *&d, size_t n, int fill) -> cudaError_t {
         using T = std::remove_reference_t<decltype(*d)>;
-        cudaError_t e = (cudaError_t)dmalloc(reinterpret_cast<void **>(&d), (n ? n : 1) * sizeof(T));
-        if (e != cudaSuccess) return e;
-        bytes += (n ? n : 1) * sizeof(T);
-        return fill >= 0 ? cudaMemsetAsync(d, fill, (n ? n : 1) * sizeof(T), s) : cudaSuccess;
+        const size_t b = (n ? n : 1) * sizeof(T);
+        const size_t ab = (b + 255) & ~(size_t)255;
+        if (plan) {
+            off += ab;
+            return cudaSuccess;
+        }
+        d = reinterpret_cast<T *>(arena + off);
+        off += ab;
+        bytes += b;
+        return fill >= 0 ? cudaMemsetAsync(d, fill, b, s) : cudaSuccess;
     };
-    // product arrays (freed by free_device on error)
-    GK(alloc(g->d_src, E + kPadE, 0), "cudaMalloc(src)");
-    GK(alloc(g->d_dst, E + kPadE, 0), "cudaMalloc(dst)");
-    GK(alloc(g->d_tr, E + kPadE, 0xFF), "cudaMalloc(tr)");
-    GK(alloc(g->d_t, (size_t)E, -1), "cudaMalloc(t)");
-    GK(alloc(g->d_hi, E + kPadE, 0), "cudaMalloc(hi)");
-    GK(alloc(g->d_eptr, 4 * ((size_t)E + kPadE), 0), "cudaMalloc(eptr)");
-    GK(alloc(g->d_out_off, (size_t)V + 1, -1), "cudaMalloc(out_off)");
-    GK(alloc(g->d_in_off, (size_t)V + 1, -1), "cudaMalloc(in_off)");
-    GK(alloc(g->d_out_ent, 2 * (N + kPadEnt), 0xFF), "cudaMalloc(out_ent)");
-    GK(alloc(g->d_in_ent, 2 * (N + kPadEnt), 0xFF), "cudaMalloc(in_ent)");
-    GK(alloc(g->d_out_ptr, 4 * (N + kPadE), 0), "cudaMalloc(out_ptr)");
-    GK(alloc(g->d_in_ptr, 4 * (N + kPadE), 0), "cudaMalloc(in_ptr)");
-    GK(alloc(g->d_perm, (size_t)E, -1), "cudaMalloc(perm)");
-    g->graph_bytes = bytes;
-    // enumeration only (mayura_enumerate): input rank of the edge behind every list position
-    // (not read by the counting kernels, so not part of graph_bytes' residency estimate)
-    GK(alloc(g->d_out_rank, N + kPadE, 0xFF), "cudaMalloc(out_rank)");
-    GK(alloc(g->d_in_rank, N + kPadE, 0xFF), "cudaMalloc(in_rank)");
+    auto product = [&]() -> mayura_status {
+        GK(alloc(g->d_src, E + kPadE, 0), "cudaMalloc(src)");
+        GK(alloc(g->d_dst, E + kPadE, 0), "cudaMalloc(dst)");
+        GK(alloc(g->d_tr, E + kPadE, 0xFF), "cudaMalloc(tr)");
+        GK(alloc(g->d_t, (size_t)E, -1), "cudaMalloc(t)");
+        GK(alloc(g->d_hi, E + kPadE, 0), "cudaMalloc(hi)");
+        GK(alloc(g->d_eptr, 4 * ((size_t)E + kPadE), 0), "cudaMalloc(eptr)");
+        GK(alloc(g->d_out_off, (size_t)V + 1, -1), "cudaMalloc(out_off)");
+        GK(alloc(g->d_in_off, (size_t)V + 1, -1), "cudaMalloc(in_off)");
+        GK(alloc(g->d_out_ent, 2 * (N + kPadEnt), 0xFF), "cudaMalloc(out_ent)");
+        GK(alloc(g->d_in_ent, 2 * (N + kPadEnt), 0xFF), "cudaMalloc(in_ent)");
+        GK(alloc(g->d_out_ptr, 4 * (N + kPadE), 0), "cudaMalloc(out_ptr)");
+        GK(alloc(g->d_in_ptr, 4 * (N + kPadE), 0), "cudaMalloc(in_ptr)");
+        GK(alloc(g->d_perm, (size_t)E, -1), "cudaMalloc(perm)");
+        g->graph_bytes = bytes;
+        // enumeration only (mayura_enumerate): input rank of the edge behind every list position
+        // (not read by the counting kernels, so not part of graph_bytes' residency estimate)
+        GK(alloc(g->d_out_rank, N + kPadE, 0xFF), "cudaMalloc(out_rank)");
+        GK(alloc(g->d_in_rank, N + kPadE, 0xFF), "cudaMalloc(in_rank)");
+        return MAYURA_OK;
+    };
+    product();
+    GK((cudaError_t)dmalloc(reinterpret_cast<void **>(&arena), off), "cudaMalloc(graph arrays)");
+    g->d_arena = arena;
+    plan = false;
+    off = 0;
+    if (mayura_status ps = product()) return ps;
     g->device_bytes += bytes;
 
     Tmp tmp;

@@ -85,6 +85,7 @@ struct mayura_graph_s {
     uint32_t *d_out_ent = nullptr, *d_in_ent = nullptr;  // uint2 {tr, nbr}
     uint32_t *d_eptr = nullptr, *d_out_ptr = nullptr, *d_in_ptr = nullptr;  // uint4
     uint32_t *d_perm = nullptr;                           // input rank of edge id (GPU-built graphs)
+    char *d_arena = nullptr;                              // the one allocation holding the arrays above
     uint32_t *d_out_rank = nullptr, *d_in_rank = nullptr; // input rank of the edge behind each list position
     uint32_t *d_enum = nullptr;                           // enumeration scratch (per-warp counts / bases)
     size_t enum_bytes = 0;

@@ -118,6 +118,36 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ------------------------------------------------------------ host binding --
+def bind_to_gpu_numa(dev_index: int):
+    """Pin this process to the CPU cores NVML reports as local to the GPU (before any pinned
+    host buffer is allocated, so its pages land on the GPU's NUMA node: the e2e H2D copies then
+    do not cross the socket interconnect).  Returns a record for the JSON line."""
+    try:
+        import pynvml
+        import torch
+        pr = torch.cuda.get_device_properties(dev_index)
+        bus = "%08X:%02X:%02X.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        n = os.cpu_count() or 1
+        mask = pynvml.nvmlDeviceGetCpuAffinity(h, (n + 63) // 64)
+        cpus = {i for i in range(n) if (mask[i // 64] >> (i % 64)) & 1}
+        before = len(os.sched_getaffinity(0))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        return {"pci_bus_id": bus, "cpus": len(cpus), "cpus_before": before}
+    except Exception as e:  # no NVML / no affinity support: leave the process unbound
+        return {"error": str(e)[:120]}
+
+
+def unbind_all_cores():
+    try:
+        os.sched_setaffinity(0, set(range(os.cpu_count() or 1)))
+    except Exception:
+        pass
+
+
 # ------------------------------------------------------------ oracle (CPU) --
 def cpu_baseline(cfg, src, dst, t, V, budget_s: float):
     """The oracle as it stands (O2, per-motif Algorithm 1, all host cores), timed on a
@@ -254,6 +284,7 @@ def main():
     assert torch.cuda.is_available(), "bench.py needs a GPU"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    binding = bind_to_gpu_numa(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     import __graft_entry__
@@ -378,7 +409,8 @@ def main():
         e2e = {"value": E / tt.item(), "unit": UNIT, "s_per_step": tt.item(), "steps_s": tsteps,
                "h2d_bytes_per_step": 16 * E, "d2h_bytes_per_step": 8 * k,
                "path": "mayura_load_graph(pinned host src/dst/t -> H2D, graph build on the GPU) + "
-                       "mayura_comine + D2H of the counts"}
+                       "mayura_comine + D2H of the counts",
+               "host_binding": binding}
 
     enum = None
     if world == 1 and not args.no_enum and not args.profile:
@@ -387,6 +419,7 @@ def main():
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        unbind_all_cores()  # the oracle baseline uses every host core
         cpu, ocounts, orng = cpu_baseline(cfg, src, dst, t, V, args.cpu_budget_s)
         if ocounts is not None:
             parity = "exact" if ocounts == got else "MISMATCH"

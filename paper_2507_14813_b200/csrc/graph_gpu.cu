@@ -208,6 +208,28 @@ __global__ void k_cuts(const unsigned long long *inc, uint32_t E, uint32_t P, un
     cut[p] = (unsigned long long)lo + 1;
 }
 
+struct SideStream {  // per device: a non-blocking stream, two events, a pinned flag word
+    std::mutex mu;
+    bool init = false;
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev2 = nullptr;
+    uint32_t *hbad = nullptr;
+};
+SideStream &side_stream(int dev) {
+    static SideStream ss[64];
+    static std::mutex init_mu;
+    SideStream &x = ss[dev & 63];
+    std::lock_guard<std::mutex> lk(init_mu);
+    if (!x.init) {
+        cudaStreamCreateWithFlags(&x.s2, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&x.ev0, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&x.ev2, cudaEventDisableTiming);
+        cudaMallocHost((void **)&x.hbad, 16);
+        x.init = true;
+    }
+    return x;
+}
+
 struct Tmp {  // scratch freed at scope exit
     std::vector<void *> p;
     template <typename T>
@@ -332,14 +354,22 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     GK(tmp.get(it, E), "cudaMalloc(tmp)");
     GK(tmp.get(bad, 4), "cudaMalloc(tmp)");
     trace("load: allocations");
-    GK(cudaMemcpyAsync(isrc, hsrc, 4ull * E, cudaMemcpyHostToDevice, s), "H2D(src)");
-    GK(cudaMemcpyAsync(idst, hdst, 4ull * E, cudaMemcpyHostToDevice, s), "H2D(dst)");
-    GK(cudaMemcpyAsync(it, ht, 8ull * E, cudaMemcpyHostToDevice, s), "H2D(t)");
-    GK(cudaMemsetAsync(bad, 0, 16, s), "memset");
+    // src/dst travel on a side stream while t is copied, reduced and sorted on the main one:
+    // the sort by time needs only t, so the second half of the H2D traffic overlaps it
+    SideStream &ss = side_stream(g->device);
+    std::unique_lock<std::mutex> side_lock(ss.mu);  // one build at a time uses this device's side stream
+    GK(cudaEventRecord(ss.ev0, s), "event");
+    GK(cudaStreamWaitEvent(ss.s2, ss.ev0, 0), "stream wait");
+    GK(cudaMemsetAsync(bad, 0, 16, ss.s2), "memset");
+    GK(cudaMemcpyAsync(isrc, hsrc, 4ull * E, cudaMemcpyHostToDevice, ss.s2), "H2D(src)");
+    GK(cudaMemcpyAsync(idst, hdst, 4ull * E, cudaMemcpyHostToDevice, ss.s2), "H2D(dst)");
     if (E) {
-        k_check_ids<<<blocks_for(E), kT, 0, s>>>(isrc, idst, E, V, bad);
+        k_check_ids<<<blocks_for(E), kT, 0, ss.s2>>>(isrc, idst, E, V, bad);
         count_launch();
     }
+    GK(cudaMemcpyAsync(ss.hbad, bad, 4, cudaMemcpyDeviceToHost, ss.s2), "D2H(check)");
+    GK(cudaEventRecord(ss.ev2, ss.s2), "event");
+    GK(cudaMemcpyAsync(it, ht, 8ull * E, cudaMemcpyHostToDevice, s), "H2D(t)");
     // time range -> key bits
     int64_t *mm;
     GK(tmp.get(mm, 2), "cudaMalloc(tmp)");
@@ -354,13 +384,14 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
         GK(cub::DeviceReduce::Min(cr, tb, it, mm, (int)E, s), "cub Min");
         GK(cub::DeviceReduce::Max(cr, tb, it, mm + 1, (int)E, s), "cub Max");
         int64_t hm[2];
-        uint32_t hbad = 0;
         GK(cudaMemcpyAsync(hm, mm, 16, cudaMemcpyDeviceToHost, s), "D2H(minmax)");
-        GK(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s), "D2H(check)");
         GK(cudaStreamSynchronize(s), "sync");
-        if (hbad) return fail(MAYURA_E_INVALID, "mayura_load_graph: vertex id >= n_vertices");
         tmin = hm[0];
         tmax = hm[1];
+    }
+    if (!E) {
+        GK(cudaEventSynchronize(ss.ev2), "event sync");
+        GK(cudaStreamWaitEvent(s, ss.ev2, 0), "stream wait");
     }
     trace("load: H2D + id check + minmax");
     // 1. stable sort by (t, input rank)
@@ -375,6 +406,10 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
         char *ct;
         GK(tmp.get(ct, need), "cudaMalloc(tmp)");
         GK(cub::DeviceRadixSort::SortPairs(ct, need, key, key2, val, g->d_perm, (int)E, 0, tbits, s), "cub sort");
+        // src/dst on the device and checked (host waits for the side stream only: the sort runs on)
+        GK(cudaEventSynchronize(ss.ev2), "event sync");
+        if (*ss.hbad) return fail(MAYURA_E_INVALID, "mayura_load_graph: vertex id >= n_vertices");
+        GK(cudaStreamWaitEvent(s, ss.ev2, 0), "stream wait");
         k_gather<<<blocks_for(E), kT, 0, s>>>(g->d_perm, isrc, idst, it, g->d_src, g->d_dst, g->d_t, E); count_launch();
         // 2. time ranks
         k_time_rank<<<blocks_for(E), kT, 0, s>>>(g->d_t, g->d_tr, E); count_launch();

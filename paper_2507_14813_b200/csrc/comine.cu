@@ -259,12 +259,13 @@ cudaError_t launch_lane(const lane::LParams &p, uint32_t max_vertices, bool stat
     return launch_lane_v<16>(p, stats, generic, s, sms);
 }
 
-// Kernel form (MAYURA_KERNEL overrides): "flat" (level-synchronous, entry-parallel; flat.cuh),
+// Kernel form (MAYURA_KERNEL overrides): "mixed" (heavy roots in the flat form, light roots
+// depth-first), "flat" (level-synchronous, entry-parallel; flat.cuh),
 // "hybrid" (one breadth-first level + the depth-first lane kernel), "lane", "bfs".  Default:
 // flat when the graph arrays fit in L2, else hybrid.  Measured (profiles/README.md r04): flat
 // C1 0.172 -> 0.076 ms, C2 0.527 -> 0.321 ms; on DRAM-resident graphs its per-level frontier
 // and window-piece traffic loses (C3 4.9 ms hybrid vs 7.8 ms flat).
-enum KernelKind { K_HYBRID = 0, K_LANE = 1, K_BFS = 2, K_FLAT = 3 };
+enum KernelKind { K_HYBRID = 0, K_LANE = 1, K_BFS = 2, K_FLAT = 3, K_MIXED = 4 };
 bool l2_resident(const mayura_graph_s *g) {
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
@@ -276,6 +277,7 @@ KernelKind kernel_kind(const mayura_graph_s *g) {  // read per call (tests switc
     if (e && std::strcmp(e, "bfs") == 0) return K_BFS;
     if (e && std::strcmp(e, "flat") == 0) return K_FLAT;
     if (e && std::strcmp(e, "hybrid") == 0) return K_HYBRID;
+    if (e && std::strcmp(e, "mixed") == 0) return K_MIXED;
     return l2_resident(g) ? K_FLAT : K_HYBRID;
 }
 // hybrid: a root is split breadth-first only if one of its root-node windows has >= this
@@ -661,7 +663,29 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
            "flat pass launch");
         return MAYURA_OK;
     }
-    if (kind == K_FLAT) levels = std::min(hybrid_levels(), dt.max_edges > 2 ? dt.max_edges - 2 : 0u);
+    if (kind == K_MIXED && !st && dt.max_edges > 2) {  // heavy roots flat, then light roots depth-first
+        const uint32_t fl = dt.max_edges - 1;
+        mayura_status bs = ensure_bfs_buffers(g, words, 2);
+        if (bs != MAYURA_OK) return bs;
+        bs = ensure_flat_win(g);
+        if (bs != MAYURA_OK) return bs;
+        uint32_t *ctl = g->d_bfs_ctl;
+        CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * kCtlTotal, s), "cudaMemsetAsync(ctl)");
+        bfs::BParams b = bfs_params(g, dt, r0, n_roots, counts, nullptr, 0u);
+        b.heavy_min = heavy_min(g);
+        b.light = g->d_light;
+        uint32_t *bufs[2] = {g->d_bfs[0], g->d_bfs[1]};
+        CK(launch_flat(b, dt.max_vertices, fl, bufs, ctl, g->bfs_seg_cap, reinterpret_cast<uint4 *>(g->d_flat_win),
+                       flat_win_cap(g, dt.max_vertices), dt.gwant, s, sms),
+           "flat pass launch");
+        lane::LParams q = lane_params(g, dt, r0, n_roots, lb, counts, nullptr, false);
+        q.light = g->d_light;
+        q.light_cnt = b.light_cnt;
+        q.heavy_min = b.heavy_min;
+        CK(launch_lane(q, dt.max_vertices, false, dt.generic, s, sms), "comine_lane_kernel launch");
+        return MAYURA_OK;
+    }
+    if (kind == K_FLAT || kind == K_MIXED) levels = std::min(hybrid_levels(), dt.max_edges > 2 ? dt.max_edges - 2 : 0u);
     lane::LParams q = lane_params(g, dt, r0, n_roots, lb, counts, stats, st);
     if (levels > 0) {
         mayura_status bs = ensure_bfs_buffers(g, words, levels >= 2 ? 2 : 1);
@@ -746,10 +770,10 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
         for (size_t i = 1; i < tabs.size(); i++) mv = std::max(mv, tabs[i].max_vertices);
         const KernelKind kind = kernel_kind(g);
         if (kind != K_LANE && n_roots > 0) {
-            const uint32_t lv = kind == K_BFS || kind == K_FLAT ? 2u : std::min(hybrid_levels(), 2u);
+            const uint32_t lv = kind == K_BFS || kind == K_FLAT || kind == K_MIXED ? 2u : std::min(hybrid_levels(), 2u);
             if (lv > 0) st = ensure_bfs_buffers(g, rec_words(mv), lv >= 2 ? 2 : 1);
             if (st != MAYURA_OK) return st;
-            if (kind == K_FLAT) st = ensure_flat_win(g);
+            if (kind == K_FLAT || kind == K_MIXED) st = ensure_flat_win(g);
             if (st != MAYURA_OK) return st;
         }
         if (g->fresh_alloc) {
@@ -1126,6 +1150,7 @@ extern "C" const char *mayura_kernel_form(mayura_graph g) {
         case K_FLAT: return "flat";
         case K_LANE: return "lane";
         case K_BFS: return "bfs";
+        case K_MIXED: return "mixed";
         default: return "hybrid";
     }
 }

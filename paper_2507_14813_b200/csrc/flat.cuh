@@ -108,6 +108,19 @@ __global__ void __launch_bounds__(kTB) flat_win_kernel(const __grid_constant__ F
             if (go && !bfs::load_root<MAXV>(p, xid, x)) go = false;
             if (go && (root.flags & NODE_COMPLETION)) bfs::count_add(c, root.slot, 1);
             if (!(root.flags & NODE_INNER)) go = false;
+            if (p.light) {  // mixed form: light roots go to the depth-first kernel whole (listed here)
+                const bool light = go && !lane::heavy_root<MAXV>(s.nodes, s.groups, root, x.P, x.h, x.m2g[0],
+                                                                x.m2g[1], p.out_off, p.out_ent, p.in_off,
+                                                                p.in_ent, p.heavy_min);
+                const unsigned lm = __ballot_sync(kFull, light);
+                if (lm) {
+                    uint32_t b = 0;
+                    if (lane_id == 0) b = atomicAdd(p.light_cnt, (uint32_t)__popc(lm));
+                    b = __shfl_sync(kFull, b, 0);
+                    if (light) p.light[b + __popc(lm & ((1u << lane_id) - 1u))] = xid;
+                }
+                go = go && !light;
+            }
         } else if (go) {
             bfs::load_rec<MAXV>(p, s.pref, item, x);
             go = x.node != bfs::kHole;

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
     const LNode root = s_nodes[0];
     const bool root_inner = (root.flags & NODE_INNER) != 0;
     const uint32_t n_pm = p.pm ? s_pref[kPmStripes] : 0u;
-    const uint32_t n_items = n_pm + (!p.pm ? p.n_roots : p.light ? *(volatile const uint32_t *)p.light_cnt : 0u);
+    const uint32_t n_items = n_pm + (p.light ? *(volatile const uint32_t *)p.light_cnt : !p.pm ? p.n_roots : 0u);
 
     // ------------------------------------------------------------ lane state
     bool active = false, scan = false, help = false, fresh = false;
@@ -403,7 +403,8 @@ __global__ void __launch_bounds__(kLB, 8) comine_lane_kernel(const __grid_consta
                     lim = kNone; d = 0; scan = false; age = 0;
                     active = true;
                 }
-            } else if (mine && p.pm) {  // hybrid: a light root, mined whole (listed by the breadth-first level)
+            } else if (mine && p.light) {  // hybrid / mixed: a light root, mined whole (listed by the
+                                           // breadth-first level, which also counted its completion)
                 const uint32_t r = __ldg(p.light + (item - n_pm));
 #pragma unroll
                 for (int k = 2; k < MAXV; k++) m2g[k] = kNone;

@@ -12,7 +12,7 @@ import synth
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["flat", "hybrid", "lane"])
+@pytest.fixture(params=["flat", "hybrid", "lane", "mixed"])
 def M(monkeypatch, request):
     import torch
     if not torch.cuda.is_available():

@@ -103,3 +103,16 @@ def test_enumerate_device_output_and_capacity(M, oracle_mod):
         M.mayura_enumerate(g.handle, tree.handle, 0, g.n_edges, None, small, need - 1)
     g.close()
     tree.close()
+
+
+def test_enumerate_edge_cases(M, oracle_mod):
+    """Empty graph, all self-loops, delta = 0: zero tuples (size query and host output)."""
+    for src, dst, t, V, delta in (([], [], [], 3, 10), ([1, 2, 2], [1, 2, 2], [1, 2, 3], 3, 10),
+                                  ([0, 1, 2], [1, 2, 0], [1, 2, 3], 3, 0)):
+        g = M.Graph(src, dst, t, V, device=0)
+        tree = M.MGTree([synth.MOTIFS["tri_cycle"], synth.MOTIFS["recip2"]], delta)
+        counts, lists = M.enumerate_matches(g, tree)
+        assert counts == [0, 0] and all(len(x) == 0 for x in lists)
+        assert M.mayura.mayura_enumerate_size(g.handle, tree.handle, 0, g.n_edges)[1] == 0
+        g.close()
+        tree.close()

@@ -67,3 +67,19 @@ def test_form_overflow_fallbacks(M, oracle_mod, monkeypatch):
     src, dst, t, V = cfg.graph()
     motifs = synth.group(synth.GROUP_C2) + [[(0, 1), (2, 3), (3, 0)]]
     assert run(M, src, dst, t, V, motifs, cfg.delta) == oracle_mod.backtrack(src, dst, t, V, motifs, cfg.delta)
+
+
+def test_form_edge_cases(M, oracle_mod):
+    """Empty graph, all self-loops, all tied timestamps, delta = 0, 2^62 timestamps, a
+    1-edge-only group (no MG-Tree level below the root) -- in every kernel form."""
+    tri = [synth.MOTIFS["tri_cycle"], synth.MOTIFS["edge1"]]
+    assert run(M, [], [], [], 3, tri, 10) == [0, 0]
+    assert run(M, [1, 2, 2], [1, 2, 2], [1, 2, 3], 3, tri, 10) == [0, 0]
+    assert run(M, [0, 1, 2], [1, 2, 0], [5, 5, 5], 3, tri, 100) == [0, 3]
+    src, dst, t, V = synth.random_graph(9, 10, 500, 100)
+    g2 = synth.group(synth.GROUP_C2)
+    assert run(M, src, dst, t, V, g2, 0) == oracle_mod.backtrack(src, dst, t, V, g2, 0)
+    big = 2 ** 62
+    assert run(M, [0, 1], [1, 0], [big, big + 5], 2, [synth.MOTIFS["recip2"]], 2 ** 62) == [1]
+    assert run(M, src, dst, t, V, [synth.MOTIFS["edge1"]], 10) == \
+        oracle_mod.backtrack(src, dst, t, V, [synth.MOTIFS["edge1"]], 10)

@@ -116,3 +116,14 @@ def test_enumerate_edge_cases(M, oracle_mod):
         assert M.mayura.mayura_enumerate_size(g.handle, tree.handle, 0, g.n_edges)[1] == 0
         g.close()
         tree.close()
+
+
+def test_enumerate_maximum_motif_size(M, oracle_mod):
+    """8-edge motifs (prefixes of up to 7 edges travel with tasks and frames), up to 16 motif
+    vertices (8 disjoint edges: every window from the edge array)."""
+    src, dst, t, V = synth.random_graph(31, 9, 500, 50, 0.0)
+    group = [[(i, i + 1) for i in range(8)], [(i, (i + 1) % 8) for i in range(8)],
+             [(0, 1), (1, 2), (2, 0), (0, 3), (3, 1), (1, 0), (2, 3), (3, 0)]]
+    assert all(check(M, oracle_mod, src, dst, t, V, group, 20))
+    src, dst, t, V = synth.random_graph(32, 40, 60, 30, 0.0)
+    assert check(M, oracle_mod, src, dst, t, V, [[(2 * i, 2 * i + 1) for i in range(8)]], 9)[0] > 0

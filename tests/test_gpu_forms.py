@@ -83,3 +83,25 @@ def test_form_edge_cases(M, oracle_mod):
     assert run(M, [0, 1], [1, 0], [big, big + 5], 2, [synth.MOTIFS["recip2"]], 2 ** 62) == [1]
     assert run(M, src, dst, t, V, [synth.MOTIFS["edge1"]], 10) == \
         oracle_mod.backtrack(src, dst, t, V, [synth.MOTIFS["edge1"]], 10)
+
+
+def test_form_maximum_motif_size(M, oracle_mod):
+    """MAYURA_MAX_EDGES = 8 edges per motif and up to 16 motif vertices (the largest register
+    class of m2g), 7 MG-Tree levels below the root: an 8-edge fan-out against its closed form
+    at 3,000 edges, and 8-edge path / cycle / fan-in / mixed motifs plus 8 disjoint edges
+    (16 vertices, every window from the edge array) against the oracle on a small graph."""
+    from tests import _pins
+    src, dst, t, V = synth.out_star(3000)
+    star8 = [(0, i) for i in range(1, 9)]
+    assert run(M, src, dst, t, V, [star8], 12) == [_pins.star_fanout_count(3000, 8, 12)]
+    src, dst, t, V = synth.random_graph(31, 9, 500, 50, 0.0)
+    path8 = [(i, i + 1) for i in range(8)]
+    cyc8 = [(i, (i + 1) % 8) for i in range(8)]
+    fanin8 = [(i, 0) for i in range(1, 9)]
+    mixed = [(0, 1), (1, 2), (2, 0), (0, 3), (3, 1), (1, 0), (2, 3), (3, 0)]
+    group = [path8, cyc8, fanin8, mixed]
+    exp = oracle_mod.backtrack(src, dst, t, V, group, 20)
+    assert all(exp) and run(M, src, dst, t, V, group, 20) == exp
+    src, dst, t, V = synth.random_graph(32, 40, 60, 30, 0.0)
+    disj = [[(2 * i, 2 * i + 1) for i in range(8)]]
+    assert run(M, src, dst, t, V, disj, 9) == oracle_mod.backtrack(src, dst, t, V, disj, 9)

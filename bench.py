@@ -282,11 +282,17 @@ def main():
     import torch
     import torch.distributed as dist
     assert torch.cuda.is_available(), "bench.py needs a GPU"
+    shared = os.environ.get("MAYURA_BENCH_SHARED_GPU") == "1"  # test hook: all ranks on cuda:0 over gloo
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     binding = bind_to_gpu_numa(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     import __graft_entry__
     if rank == 0 and __graft_entry__._builder()._stale():
         __graft_entry__._builder().build()

@@ -49,6 +49,7 @@ __device__ __forceinline__ void pdl_begin() {
 #include "lane.cuh"
 #include "bfs.cuh"
 #include "flat.cuh"
+#include "flat_enum.cuh"
 
 // a2: hi[r] = (last edge id e with t[e] <= t[r] + delta), by galloping from r (windows
 // are short) then binary search.  Also zeroes the load-balancer words and the output
@@ -829,6 +830,102 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
     return MAYURA_OK;
 }
 
+// ---- enumeration in the flat form (graphs that fit in L2): window + entry pass per level
+template <int MAXV>
+cudaError_t launch_flat_enum_v(flat::EParams e, uint32_t levels, uint32_t *bufs[2], uint32_t *ctl, uint32_t seg_cap,
+                               uint32_t win_cap, cudaStream_t s, int sms) {
+    constexpr int PW = flat::EPiece<MAXV>::W / 4;
+    (void)PW;
+    const size_t smem = bfs::smem_bytes(e.b.n_nodes, e.b.n_groups, e.b.n_slots, flat::kTB);
+    e.win_seg_cap = win_cap / bfs::kStripes;
+    auto launch = [&](auto kern, bool roots) -> cudaError_t {
+        cudaError_t er = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (er != cudaSuccess) return er;
+        int per_sm = 0;
+        er = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, flat::kTB, smem);
+        if (er != cudaSuccess) return er;
+        uint32_t grid = (uint32_t)(sms * (per_sm > 0 ? per_sm : 1));
+        if (roots) grid = std::max(1u, std::min(grid, (e.b.n_roots + flat::kTB - 1) / flat::kTB));
+        er = launch_pdl(kern, grid, flat::kTB, smem, s, e);
+        count_launch();
+        return er != cudaSuccess ? er : cudaGetLastError();
+    };
+    if (levels == 0) {  // 1-edge motifs only: root completions
+        e.win_cnt = ctl + kCtlFlat;
+        return launch(flat::flat_enum_win_kernel<MAXV, true>, true);
+    }
+    for (uint32_t L = 0; L < levels; L++) {
+        e.b.in.data = L ? bufs[(L - 1) & 1] : nullptr;
+        e.b.in.cnt = L ? ctl + (L - 1) * kCtlWords : nullptr;
+        e.b.in.seg_cap = seg_cap;
+        e.b.out.data = bufs[L & 1];
+        e.b.out.cnt = ctl + L * kCtlWords;
+        e.b.out.seg_cap = seg_cap;
+        e.win_cnt = ctl + kCtlFlat + L * bfs::kStripes;
+        cudaError_t er = L == 0 ? launch(flat::flat_enum_win_kernel<MAXV, true>, true)
+                                : launch(flat::flat_enum_win_kernel<MAXV, false>, false);
+        if (er == cudaSuccess) er = launch(flat::flat_enum_entry_kernel<MAXV>, false);
+        if (er != cudaSuccess) return er;
+    }
+    return cudaSuccess;
+}
+
+uint32_t erec_words(uint32_t mv) {
+    return mv <= 4 ? flat::ERec<4>::W : mv <= 6 ? flat::ERec<6>::W : mv <= 8 ? flat::ERec<8>::W : flat::ERec<16>::W;
+}
+uint32_t epiece_bytes(uint32_t mv) {
+    return 4 * (mv <= 4 ? flat::EPiece<4>::W : mv <= 6 ? flat::EPiece<6>::W : mv <= 8 ? flat::EPiece<8>::W
+                                                                                      : flat::EPiece<16>::W);
+}
+
+// Flat-form enumeration attempt.  Returns MAYURA_OK with *done = true when the tuples are in
+// `dout` (device); *done = false when a buffer overflowed (the caller re-runs depth-first).
+mayura_status flat_enum(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32_t n_roots,
+                        const std::vector<unsigned long long> &slot_word, uint32_t *dout, cudaStream_t s, bool *done) {
+    *done = false;
+    const uint32_t ns = dt.n_slots, mv = dt.max_vertices;
+    mayura_status st = ensure_bfs_buffers(g, erec_words(mv), 2);
+    if (st == MAYURA_OK) st = ensure_flat_win(g);
+    if (st != MAYURA_OK) return st;
+    unsigned long long *sc = nullptr;  // cursor[ns] | slot_word[ns] | overflow
+    CK((cudaError_t)dmalloc((void **)&sc, 16 * (size_t)ns + 16), "cudaMalloc(enumeration cursors)");
+    CK(cudaStreamSynchronize(0), "cudaStreamSynchronize");
+    uint32_t *ovf = reinterpret_cast<uint32_t *>(sc + 2 * ns);
+    mayura_status rs = MAYURA_OK;
+    cudaError_t e = cudaMemsetAsync(sc, 0, 16 * (size_t)ns + 16, s);
+    if (e == cudaSuccess && ns) e = cudaMemcpyAsync(sc + ns, slot_word.data(), 8 * (size_t)ns, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(g->d_bfs_ctl, 0, sizeof(uint32_t) * kCtlTotal, s);
+    if (e == cudaSuccess) {
+        flat::EParams ep;
+        ep.b = bfs_params(g, dt, r0, n_roots, nullptr, nullptr, 0u);
+        ep.win = reinterpret_cast<uint4 *>(g->d_flat_win);
+        ep.perm = g->d_perm;
+        ep.out_rank = g->d_out_rank;
+        ep.in_rank = g->d_in_rank;
+        ep.out = dout;
+        ep.slot_word = sc + ns;
+        ep.cursor = sc;
+        ep.overflow = ovf;
+        uint32_t *bufs[2] = {g->d_bfs[0], g->d_bfs[1]};
+        const uint32_t levels = dt.max_edges > 1 ? dt.max_edges - 1 : 0;
+        uint64_t wc = std::min<uint64_t>(g->flat_win_bytes / epiece_bytes(mv), 0xFFFFFFFFull);
+        if (const char *ev = getenv("MAYURA_FLAT_WIN_CAP")) wc = std::min<uint64_t>(wc, (uint64_t)std::max(1L, atol(ev)));
+        const uint32_t wcap = (uint32_t)wc;  // (MAYURA_FLAT_WIN_CAP: test hook forcing the fallback)
+        const int sms = sm_count(g->device);
+        if (mv <= 4) e = launch_flat_enum_v<4>(ep, levels, bufs, g->d_bfs_ctl, g->bfs_seg_cap, wcap, s, sms);
+        else if (mv <= 6) e = launch_flat_enum_v<6>(ep, levels, bufs, g->d_bfs_ctl, g->bfs_seg_cap, wcap, s, sms);
+        else if (mv <= 8) e = launch_flat_enum_v<8>(ep, levels, bufs, g->d_bfs_ctl, g->bfs_seg_cap, wcap, s, sms);
+        else e = launch_flat_enum_v<16>(ep, levels, bufs, g->d_bfs_ctl, g->bfs_seg_cap, wcap, s, sms);
+    }
+    uint32_t hov = 1;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hov, ovf, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rs = cuda_fail(e, "flat enumeration");
+    dfree(sc);
+    if (rs == MAYURA_OK) *done = hov == 0;
+    return rs;
+}
+
 // Enumeration (NEXT-3; "a comprehensive list of all matching motifs
 // (enumeration)", :412-413; Algo 1 l.201 / Algo 3 l.662 "add to the enumeration list").
 // Two passes of the depth-first lane kernel over the same static root-to-warp mapping:
@@ -862,6 +959,51 @@ mayura_status run_enum(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint6
         if (first_of[slot_of[q]] == kNone) first_of[slot_of[q]] = q;
     }
     const uint32_t n_roots = (uint32_t)(re - rb);
+    // graphs that fit in L2: the flat form (counts from the flat counting pass, then one
+    // enumeration pass per level); a full buffer falls back to the depth-first form below
+    if (kernel_kind(g) == K_FLAT && n_roots > 0 && !getenv("MAYURA_ENUM_LANE")) {
+        std::vector<uint64_t> cnt(k, 0);
+        st = run(g, m, rb, re, stream, cnt.data(), 0, 0, nullptr);
+        if (st != MAYURA_OK) return st;
+        for (uint32_t i = 0; i < k; i++) counts_out[i] = cnt[i];
+        std::vector<uint64_t> word(k + 1, 0);
+        for (uint32_t i = 0; i < k; i++) word[i + 1] = word[i] + cnt[i] * (uint64_t)m->canon[i].size();
+        if (words_needed) *words_needed = word[k];
+        if (!out) return MAYURA_OK;
+        if (cap_words < word[k]) return fail(MAYURA_E_LIMIT, "mayura_enumerate: capacity_words < words needed");
+        if (word[k] == 0) return MAYURA_OK;
+        std::vector<unsigned long long> sw(ns, 0);
+        for (uint32_t sl = 0; sl < ns; sl++) sw[sl] = first_of[sl] == kNone ? 0 : word[first_of[sl]];
+        uint32_t *dout = out;
+        if (!on_device) {
+            CK((cudaError_t)dmalloc((void **)&dout, 4 * word[k]), "cudaMalloc(enumeration staging)");
+            CK(cudaStreamSynchronize(0), "cudaStreamSynchronize");
+        }
+        bool done = false;
+        mayura_status fs = flat_enum(g, dt, (uint32_t)rb, n_roots, sw, dout, s, &done);
+        if (fs == MAYURA_OK && done) {
+            cudaError_t e = cudaSuccess;
+            for (uint32_t i = 0; i < k && e == cudaSuccess; i++) {  // duplicate motifs: copy the first one's tuples
+                const uint32_t q0 = first_of[slot_of[i]];
+                if (q0 != i && cnt[i])
+                    e = cudaMemcpyAsync(dout + word[i], dout + word[q0], 4 * cnt[i] * m->canon[i].size(),
+                                        cudaMemcpyDeviceToDevice, s);
+            }
+            if (e == cudaSuccess && !on_device) e = cudaMemcpyAsync(out, dout, 4 * word[k], cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (!on_device) {
+                dfree(dout);
+                cudaStreamSynchronize(0);
+            }
+            return e == cudaSuccess ? MAYURA_OK : cuda_fail(e, "flat enumeration output");
+        }
+        if (!on_device) {
+            dfree(dout);
+            cudaStreamSynchronize(0);
+        }
+        if (fs != MAYURA_OK) return fs;
+        // overflow: fall through to the depth-first form
+    }
     const int sms = sm_count(g->device);
     lane::LParams q = lane_params(g, dt, (uint32_t)rb, n_roots, nullptr, nullptr, nullptr, false);
     uint32_t grid = 0;

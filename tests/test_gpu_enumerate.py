@@ -11,11 +11,19 @@ import synth
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def M():
+@pytest.fixture(params=["flat", "lane", "flat-overflow"])
+def M(request, monkeypatch):
+    """Small graphs enumerate in the flat form by default; MAYURA_ENUM_LANE=1 forces the
+    depth-first form; tiny piece / frontier capacities make the flat attempt overflow and
+    fall back to the depth-first form."""
     import torch
     if not torch.cuda.is_available():
         pytest.fail("GPU tests need a CUDA device")
+    if request.param == "lane":
+        monkeypatch.setenv("MAYURA_ENUM_LANE", "1")
+    if request.param == "flat-overflow":
+        monkeypatch.setenv("MAYURA_FLAT_WIN_CAP", "70")
+        monkeypatch.setenv("MAYURA_BFS_SEG_CAP", "2")
     import paper_2507_14813_b200 as M
     return M
 

@@ -267,7 +267,10 @@ def enumeration_leg(M, g, tree, cfg, src, dst, t, V, sp, stream, st, peak, got, 
                          "note": "2 traversal passes (B_alg each) + 4 B per output word; includes the mid-call "
                                  "host sync that sizes the output"},
             "parity_vs_oracle": parity,
-            "path": "mayura_enumerate(device output): count pass per warp, CUB scan, write pass"}
+            "path": ("mayura_enumerate(device output), flat form: flat counting pass, then a window + entry "
+                     "pass per MG-Tree level writing tuples" if M.mayura_kernel_form(g.handle) == "flat" else
+                     "mayura_enumerate(device output), depth-first form: per-warp count pass, CUB scan, "
+                     "write pass")}
 
 
 def main():

@@ -961,7 +961,7 @@ mayura_status run_enum(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint6
     const uint32_t n_roots = (uint32_t)(re - rb);
     // graphs that fit in L2: the flat form (counts from the flat counting pass, then one
     // enumeration pass per level); a full buffer falls back to the depth-first form below
-    if (kernel_kind(g) == K_FLAT && n_roots > 0 && !getenv("MAYURA_ENUM_LANE")) {
+    if (n_roots > 0 && !getenv("MAYURA_ENUM_LANE")) {
         std::vector<uint64_t> cnt(k, 0);
         st = run(g, m, rb, re, stream, cnt.data(), 0, 0, nullptr);
         if (st != MAYURA_OK) return st;

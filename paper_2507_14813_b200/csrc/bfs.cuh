@@ -45,6 +45,10 @@ struct Front {
 
 struct BParams {
     const uint32_t *src, *dst, *tr, *hi;
+    const int64_t *T;        // flat form: timestamps, so its level-0 pass computes hi (else null)
+    int64_t delta;
+    uint32_t E;
+    uint32_t *hi_w;          // hi, writable (the flat level-0 pass stores what it computed)
     const uint4 *eptr;
     const uint32_t *out_off, *in_off;
     const uint2 *out_ent, *in_ent;

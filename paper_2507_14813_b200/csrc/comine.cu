@@ -46,6 +46,30 @@ __device__ __forceinline__ void pdl_begin() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// hi(r) = last edge id with T <= T[r] + delta: galloping from r (windows are
+// short) then binary search
+__device__ __forceinline__ uint32_t window_end_of(const int64_t *__restrict__ T, uint32_t E, int64_t delta, uint32_t r) {
+    const int64_t x = __ldg(T + r);
+    const int64_t lim = (delta > INT64_MAX - x) ? INT64_MAX : x + delta;
+    uint32_t a = r + 1, step = 1;  // invariant: T[a-1] <= lim
+    uint32_t b = E;
+    while (a < E) {
+        const uint32_t probe = min(E - 1, a + step - 1);
+        if (__ldg(T + probe) > lim) {
+            b = probe;
+            break;
+        }
+        a = probe + 1;
+        step <<= 1;
+    }
+    while (a < b) {  // first index in [a, b) with T > lim
+        const uint32_t m = a + ((b - a) >> 1);
+        if (__ldg(T + m) > lim) b = m;
+        else a = m + 1;
+    }
+    return a - 1;
+}
+
 #include "lane.cuh"
 #include "bfs.cuh"
 #include "flat.cuh"
@@ -63,25 +87,7 @@ __global__ void window_end_kernel(const int64_t *__restrict__ T, uint32_t E, int
     if (tid < n_counts) counts[tid] = 0;
     for (uint32_t k = tid; k < n_roots; k += gridDim.x * blockDim.x) {
         const uint32_t r = r0 + k;
-        const int64_t x = __ldg(T + r);
-        const int64_t lim = (delta > INT64_MAX - x) ? INT64_MAX : x + delta;
-        uint32_t a = r + 1, step = 1;  // invariant: T[a-1] <= lim
-        uint32_t b = E;
-        while (a < E) {
-            const uint32_t probe = min(E - 1, a + step - 1);
-            if (__ldg(T + probe) > lim) {
-                b = probe;
-                break;
-            }
-            a = probe + 1;
-            step <<= 1;
-        }
-        while (a < b) {  // first index in [a, b) with T > lim
-            const uint32_t m = a + ((b - a) >> 1);
-            if (__ldg(T + m) > lim) b = m;
-            else a = m + 1;
-        }
-        hi[r] = a - 1;
+        hi[r] = window_end_of(T, E, delta, r);
     }
 }
 
@@ -634,6 +640,10 @@ bfs::BParams bfs_params(const mayura_graph_s *g, const DeviceTable &dt, uint32_t
     b.fallback = g->d_bfs_ctl + kCtlWords * bfs::kMaxLevels;
     b.inline_preleaf = inline_preleaf;
     b.heavy_min = 0;  // set by mine() for the hybrid's single breadth-first level
+    b.T = nullptr;    // set by the flat path: its level-0 pass computes (and stores) hi itself
+    b.delta = 0;
+    b.E = (uint32_t)g->E;
+    b.hi_w = g->d_hi;
     b.light = nullptr;
     b.light_cnt = g->d_bfs_ctl + kCtlWords * bfs::kMaxLevels + 1;
     b.counts = counts; b.stats = stats;
@@ -642,7 +652,7 @@ bfs::BParams bfs_params(const mayura_graph_s *g, const DeviceTable &dt, uint32_t
 
 // One co-mining pass of table dt over roots [r0, r0 + n_roots) into counts (already zeroed).
 mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32_t n_roots, uint32_t *lb,
-                   unsigned long long *counts, unsigned long long *stats, cudaStream_t s, int sms) {
+                   unsigned long long *counts, unsigned long long *stats, cudaStream_t s, int sms, int64_t delta) {
     const bool st = stats != nullptr;
     const KernelKind kind = kernel_kind(g);
     const uint32_t words = rec_words(dt.max_vertices);
@@ -658,6 +668,8 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         uint32_t *ctl = g->d_bfs_ctl;
         CK(cudaMemsetAsync(ctl, 0, sizeof(uint32_t) * kCtlTotal, s), "cudaMemsetAsync(ctl)");
         bfs::BParams b = bfs_params(g, dt, r0, n_roots, counts, nullptr, 0u);
+        b.T = g->d_t;  // no window_end_kernel before the flat form: level 0 computes hi
+        b.delta = delta;
         uint32_t *bufs[2] = {g->d_bfs[0], g->d_bfs[1]};
         CK(launch_flat(b, dt.max_vertices, fl, bufs, ctl, g->bfs_seg_cap, reinterpret_cast<uint4 *>(g->d_flat_win),
                        flat_win_cap(g, dt.max_vertices), dt.gwant, s, sms),
@@ -784,7 +796,11 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
     }
     trace("comine: tables + scratch");
     const uint32_t n_lb = (uint32_t)(LB_N * n_launch);
-    {
+    // the flat form computes hi in its level-0 pass and uses no scheduler words: only the
+    // counts need zeroing (one memset instead of the window_end_kernel launch)
+    const bool flat_only = kernel_kind(g) == K_FLAT && !stats_host && tabs[0].max_edges > 1;
+    if (flat_only) CK(cudaMemsetAsync(d_counts, 0, sizeof(unsigned long long) * k, s), "cudaMemsetAsync(counts)");
+    if (!flat_only) {
         const int threads = 256;
         uint32_t blocks = (n_roots + threads - 1) / threads;
         const uint32_t minb = (std::max(n_lb, k) + threads - 1) / threads;
@@ -802,7 +818,7 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
         for (size_t i = 0; i < n_launch; i++) {
             const DeviceTable &dt = mode == 1 ? tabs[1 + i] : tabs[0];
             st = mine(g, dt, (uint32_t)rb, n_roots, g->d_queue + LB_N * i, d_counts + (mode == 1 ? i : 0),
-                      stats_host ? g->d_stats : nullptr, s, sms);
+                      stats_host ? g->d_stats : nullptr, s, sms, m->delta);
             if (st != MAYURA_OK) return st;
         }
     }

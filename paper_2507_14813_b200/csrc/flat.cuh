@@ -106,6 +106,10 @@ __global__ void __launch_bounds__(kTB) flat_win_kernel(const __grid_constant__ F
         if (L0) {
             xid = p.r0 + item;
             if (go && !bfs::load_root<MAXV>(p, xid, x)) go = false;
+            if (go && p.T) {  // hi(root) computed here (no window_end_kernel) and kept for later passes
+                x.h = window_end_of(p.T, p.E, p.delta, xid);
+                p.hi_w[xid] = x.h;
+            }
             if (go && (root.flags & NODE_COMPLETION)) bfs::count_add(c, root.slot, 1);
             if (!(root.flags & NODE_INNER)) go = false;
             if (p.light) {  // mixed form: light roots go to the depth-first kernel whole (listed here)

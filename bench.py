@@ -447,8 +447,8 @@ def main():
                "co_mining_time_s": ms_step * 1e-3, "counts": dict(zip(cfg.motifs, got)),
                "parity_vs_oracle": parity,
                "gpu_launches": launches * world,
-               "gpu_launches_detail": "mayura_launch_count() over the timed steps x ranks: per step "
-                                      "window_end_kernel + " + KERNELS.get(form, form),
+               "gpu_launches_detail": "mayura_launch_count() over the timed steps x ranks: per step " +
+                                      ("" if form == "flat" else "window_end_kernel + ") + KERNELS.get(form, form),
                "roofline": roofline, "clocks": clocks, "e2e": e2e, "independent_gpu": indep,
                "cpu_baseline": cpu, "search_stats": st, "enumeration": enum}
         print(json.dumps(out), flush=True)

@@ -268,7 +268,7 @@ def enumeration_leg(M, g, tree, cfg, src, dst, t, V, sp, stream, st, peak, got, 
                                  "host sync that sizes the output"},
             "parity_vs_oracle": parity,
             "path": ("mayura_enumerate(device output), flat form: flat counting pass, then a window + entry "
-                     "pass per MG-Tree level writing tuples" if M.mayura_kernel_form(g.handle) == "flat" else
+                     "pass per MG-Tree level writing tuples" if M.mayura_enum_form(g.handle) == "flat" else
                      "mayura_enumerate(device output), depth-first form: per-warp count pass, CUB scan, "
                      "write pass")}
 

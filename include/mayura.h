@@ -239,6 +239,13 @@ mayura_status mayura_partition_roots(mayura_graph g, int64_t delta, uint32_t n_p
  * forms return identical counts.  Static string. */
 const char *mayura_kernel_form(mayura_graph g);
 
+/* Form the last mayura_enumerate call on this graph took (enumeration row):
+ * "flat" (the flat counting pass, then a window + entry pass per MG-Tree level writing
+ * tuples), "depth-first" (per-warp count pass, CUB scan, write pass; used when
+ * MAYURA_ENUM_LANE is set or a flat buffer overflowed), or "none" (NULL graph, or no
+ * enumeration has written tuples yet).  Host-only, no CUDA call.  Static string. */
+const char *mayura_enum_form(mayura_graph g);
+
 /* Thread-local message for the last failing call on this thread ("" if none). */
 const char *mayura_last_error(void);
 

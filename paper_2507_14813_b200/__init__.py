@@ -11,4 +11,5 @@ from .mayura import (Graph, MGTree, MayuraError, comine, comine_stats, mine_inde
                      mayura_free_mgtree, mayura_graph_export, mayura_graph_export_succ, mayura_graph_info, mayura_last_error,
                      mayura_load_graph, mayura_mgtree_dump, mayura_mgtree_info, mayura_mine_independent,
                      mayura_partition_roots, mayura_version, mayura_launch_count, STATS_FIELDS,
-                     mayura_enumerate, enumerate_matches, split_tuples, mayura_comine_heuristic, mayura_kernel_form)
+                     mayura_enumerate, enumerate_matches, split_tuples, mayura_comine_heuristic, mayura_kernel_form,
+                     mayura_enum_form)

@@ -998,6 +998,7 @@ mayura_status run_enum(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint6
         bool done = false;
         mayura_status fs = flat_enum(g, dt, (uint32_t)rb, n_roots, sw, dout, s, &done);
         if (fs == MAYURA_OK && done) {
+            g->last_enum_form = "flat";
             cudaError_t e = cudaSuccess;
             for (uint32_t i = 0; i < k && e == cudaSuccess; i++) {  // duplicate motifs: copy the first one's tuples
                 const uint32_t q0 = first_of[slot_of[i]];
@@ -1020,6 +1021,7 @@ mayura_status run_enum(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint6
         if (fs != MAYURA_OK) return fs;
         // overflow: fall through to the depth-first form
     }
+    g->last_enum_form = "depth-first";
     const int sms = sm_count(g->device);
     lane::LParams q = lane_params(g, dt, (uint32_t)rb, n_roots, nullptr, nullptr, nullptr, false);
     uint32_t grid = 0;
@@ -1300,6 +1302,10 @@ extern "C" mayura_status mayura_enumerate(mayura_graph g, mayura_mgtree m, uint6
     clear_error();
     return run_enum(g, m, root_begin, root_end, cuda_stream, tuples_out, capacity_words, tuples_on_device,
                     counts_out, words_needed);
+}
+
+extern "C" const char *mayura_enum_form(mayura_graph g) {
+    return g ? g->last_enum_form : "none";
 }
 
 extern "C" const char *mayura_kernel_form(mayura_graph g) {

@@ -69,6 +69,7 @@ struct mayura_graph_s {
     int device = -1;
     bool host_built = true;                 // false: built on the GPU, host arrays made lazily
     bool fresh_alloc = false;               // device scratch allocated since the last stream sync
+    const char *last_enum_form = "none";   // form of the last mayura_enumerate (mayura_enum_form)
     // host build results (edge id order)
     std::vector<uint32_t> src, dst, tr;
     std::vector<int64_t> t;

@@ -49,6 +49,7 @@ SIGNATURES = {
     "mayura_comine_heuristic": ([_P, _P, _P, _P, _P], _int),
     "mayura_last_error": ([], ctypes.c_char_p),
     "mayura_kernel_form": ([_P], ctypes.c_char_p),
+    "mayura_enum_form": ([_P], ctypes.c_char_p),
     "mayura_version": ([], ctypes.c_char_p),
     "mayura_launch_count": ([], _u64),
 }
@@ -93,6 +94,10 @@ def mayura_version() -> str:
 
 def mayura_kernel_form(g: int) -> str:
     return _lib.mayura_kernel_form(g).decode()
+
+
+def mayura_enum_form(g: int) -> str:
+    return _lib.mayura_enum_form(g).decode()
 
 
 def mayura_launch_count() -> int:

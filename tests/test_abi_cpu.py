@@ -194,3 +194,5 @@ def test_kernel_form_host_only_graph(M):
     g = M.Graph(np.array([0, 1], np.uint32), np.array([1, 2], np.uint32), np.array([1, 2], np.int64), 3, device=-1)
     assert M.mayura_kernel_form(g.handle) == "none"
     assert M.mayura_kernel_form(None) == "none"
+    assert M.mayura_enum_form(g.handle) == "none"
+    assert M.mayura_enum_form(None) == "none"

@@ -135,3 +135,18 @@ def test_enumerate_maximum_motif_size(M, oracle_mod):
     assert all(check(M, oracle_mod, src, dst, t, V, group, 20))
     src, dst, t, V = synth.random_graph(32, 40, 60, 30, 0.0)
     assert check(M, oracle_mod, src, dst, t, V, [[(2 * i, 2 * i + 1) for i in range(8)]], 9)[0] > 0
+
+
+def test_enum_form_reports_the_form_that_ran(M, request):
+    """mayura_enum_form names the form the last enumeration took: flat by default, depth-first
+    when forced or when a flat buffer overflowed (C1: the tiny capacities overflow)."""
+    cfg = synth.CONFIGS["C1"]
+    src, dst, t, V = cfg.graph()
+    g = M.Graph(src, dst, t, V, device=0)
+    tree = M.MGTree(cfg.group(), cfg.delta)
+    assert M.mayura_enum_form(g.handle) == "none"
+    M.enumerate_matches(g, tree)
+    want = {"flat": "flat", "lane": "depth-first", "flat-overflow": "depth-first"}[request.node.callspec.params["M"]]
+    assert M.mayura_enum_form(g.handle) == want
+    g.close()
+    tree.close()

@@ -56,7 +56,10 @@ def launches(path):
 
 
 def ncu_raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # exported on the box (`ncu -i … --page raw --csv`) when the report was too big
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
         return []
@@ -79,8 +82,9 @@ def main():
                     f.write(txt[-1] + "\n")
                 r = d["roofline"]
                 lines += ["## bench line (CUDA events, not under ncu)", "",
-                          "- value: %.4g %s, ms_per_step %.4f, comine_kernel %.4f ms, window_end %.4f ms" % (
-                              d["value"], d["unit"], d["ms_per_step"], r["kernel_ms"], r["window_end_kernel_ms"]),
+                          "- value: %.4g %s, ms_per_step %.4f, co-mining pass %.4f ms (form %s), window_end_kernel %s ms" % (
+                              d["value"], d["unit"], d["ms_per_step"], r["kernel_ms"], r.get("kernel_form"),
+                              r.get("window_end_kernel_ms")),
                           "- roofline: B_alg %.4g B/launch (%.1f B/root) → %.1f GB/s = %.4f of %.1f GB/s (%s)" % (
                               r["bytes_alg_per_launch"], r["bytes_alg_per_root"], r["achieved"], r["frac"],
                               r["peak"], r["peak_source"]),
@@ -102,6 +106,8 @@ def main():
                 lines.append("| `%s` | %d | %.4f | %.1f%% |" % (k[:90], len(v), sum(v) / len(v), 100 * sum(v) / tot))
             lines.append("")
         rp = os.path.join(OUT, "prof_%s_%s.ncu-rep" % (c, tag))
+        if not os.path.exists(rp):
+            rp = os.path.join(OUT, "prof_%s_%s_raw.csv" % (c, tag))
         if os.path.exists(rp):
             for d, u in ncu_raw(rp):
                 lines += ["## `ncu --set full` of `%s`" % d.get("Kernel Name", "?")[:100], "",

@@ -413,14 +413,17 @@ mayura_status ensure_bfs_buffers(mayura_graph_s *g, uint32_t words, int nbufs) {
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     const size_t rec_bytes = (size_t)words * 4;
-    const uint64_t by_mem = (uint64_t)((free_b + (size_t)nbufs * g->bfs_bytes) * 0.4) / (rec_bytes * nbufs);
+    // the buffers held now are freed before the new ones are allocated: count them as free
+    const uint64_t by_mem = (uint64_t)((free_b + (size_t)g->bfs_nbufs * g->bfs_bytes) * 0.4) / (rec_bytes * nbufs);
     const uint64_t recs = std::max<uint64_t>(1u << 20, std::min<uint64_t>({16 * g->E, by_mem, 0xFFFFFFFFull}));
     uint32_t seg_cap = (uint32_t)((recs + bfs::kStripes - 1) / bfs::kStripes);
     // test hook: tiny capacities force the depth-first fallback / in-place long windows
     if (const char *e = getenv("MAYURA_BFS_SEG_CAP")) seg_cap = (uint32_t)std::max(1L, atol(e));
     const size_t bytes = (size_t)seg_cap * bfs::kStripes * rec_bytes;
     if (g->bfs_bytes < bytes || (nbufs == 2 && !g->d_bfs[1])) {
-        const size_t want = std::max(bytes, g->bfs_bytes);
+        // keep the old size only when the buffer count is unchanged (two buffers of a size
+        // budgeted for one would take 80 % of the device)
+        const size_t want = g->bfs_nbufs >= nbufs ? std::max(bytes, g->bfs_bytes) : bytes;
         for (int i = 0; i < 2; i++)
             if (g->d_bfs[i]) dfree(g->d_bfs[i]), g->d_bfs[i] = nullptr;
         g->device_bytes -= g->bfs_nbufs * g->bfs_bytes;

@@ -8,7 +8,7 @@ the per-motif u64 counts when N > 1).  Inputs are resident in HBM; L2 (126 MB)
 is flushed by a 512 MiB write between timed steps; per-step device time comes
 from CUDA events on the launching stream; the job time is the max over ranks.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl mayura|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl mayura|reference]
     torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
 
 Also reported: e2e (the public C-ABI path from host edge arrays: host build +
@@ -43,7 +43,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["mayura", "reference"], default="mayura")
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4",
+                    help="workload (synth.CONFIGS); default C4, the largest single-GPU config")
     ap.add_argument("--flush-mb", type=int, default=512)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -51,6 +52,7 @@ def parse():
     ap.add_argument("--no-indep", action="store_true")
     ap.add_argument("--no-enum", action="store_true", help="skip the enumeration (NEXT-3) leg")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--cpu-chunks", type=int, default=32, help="evenly spaced root chunks of the oracle sample")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no extras")
     return ap.parse_args()
 
@@ -149,49 +151,117 @@ def unbind_all_cores():
 
 
 # ------------------------------------------------------------ oracle (CPU) --
-def cpu_baseline(cfg, src, dst, t, V, budget_s: float):
-    """The oracle as it stands (O2, per-motif Algorithm 1, all host cores), timed on a
-    bounded sample of the workload: the full root range if one pass fits the budget,
-    else a contiguous root range scaled to ~budget_s.  Returns (record, counts or None)."""
+def cpu_info():
+    """Host CPU record for the baseline line: model, sockets, physical and logical cores."""
+    rec = {"logical": os.cpu_count() or 1}
+    try:
+        phys, sockets, model = set(), set(), None
+        cur = {}
+        with open("/proc/cpuinfo") as f:
+            for line in f.read().splitlines() + [""]:
+                if not line.strip():
+                    if cur:
+                        sockets.add(cur.get("physical id", "0"))
+                        phys.add((cur.get("physical id", "0"), cur.get("core id", cur.get("processor"))))
+                        model = model or cur.get("model name")
+                    cur = {}
+                    continue
+                k, _, v = line.partition(":")
+                cur[k.strip()] = v.strip()
+        rec.update({"model": model, "sockets": len(sockets), "physical": len(phys)})
+    except OSError as e:
+        rec["error"] = str(e)[:80]
+    try:
+        rec["affinity"] = len(os.sched_getaffinity(0))
+    except Exception:
+        pass
+    return rec
+
+
+def chunk_ranges(E: int, n_chunks: int, size: int):
+    """n_chunks root ranges of `size` roots, evenly spaced over [0, E) (the
+    oracle's C4/C5 sample is evenly spaced chunks, not one contiguous range)."""
+    size = max(1, min(size, E // max(1, n_chunks)))
+    if size * n_chunks >= E:
+        return [(0, E)]
+    stride = E / n_chunks
+    return [(int(i * stride + (stride - size) / 2), int(i * stride + (stride - size) / 2) + size)
+            for i in range(n_chunks)]
+
+
+def oracle_on_ranges(oracle, cfg, src, dst, t, V, ranges, threads):
+    tot = None
+    per = []
+    for a, b in ranges:
+        c = oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=(a, b), threads=threads)
+        per.append(c)
+        tot = c if tot is None else [x + y for x, y in zip(tot, c)]
+    return tot, per
+
+
+def plan_sample(oracle, cfg, src, dst, t, V, budget_s: float, n_chunks: int, threads: int):
+    """Chunks sized so one oracle pass over all of them takes ~budget_s (probed on 64-root chunks
+    at the same evenly spaced positions); the full workload if that fits the budget."""
+    E = len(src)
+    probe = chunk_ranges(E, n_chunks, 64)
+    t0 = time.perf_counter()
+    oracle_on_ranges(oracle, cfg, src, dst, t, V, probe, threads)
+    n_probe = sum(b - a for a, b in probe)
+    per_root = (time.perf_counter() - t0) / max(1, n_probe)
+    if per_root * E <= budget_s:
+        return [(0, E)]
+    size = max(16, int(budget_s / max(per_root, 1e-12) / n_chunks))
+    return chunk_ranges(E, n_chunks, size)
+
+
+def describe_sample(ranges, E, n_motifs):
+    if ranges == [(0, E)]:
+        return "full workload (all %d roots, all %d motifs, mined independently)" % (E, n_motifs)
+    n = sum(b - a for a, b in ranges)
+    return ("%d evenly spaced root chunks of %d roots (%d of %d roots, %.3f%%; first [%d, %d), last [%d, %d)), "
+            "all %d motifs mined independently" % (len(ranges), ranges[0][1] - ranges[0][0], n, E, 100.0 * n / E,
+                                                   ranges[0][0], ranges[0][1], ranges[-1][0], ranges[-1][1], n_motifs))
+
+
+def cpu_baseline(cfg, src, dst, t, V, budget_s: float, n_chunks: int):
+    """The oracle as it stands (O2, per-motif Algorithm 1, all host cores), timed on a bounded
+    sample of the workload: the whole root range if one pass fits the budget, else n_chunks
+    evenly spaced root chunks scaled to ~budget_s.  Returns (record, per-chunk counts, ranges)."""
     import oracle
     threads = os.cpu_count() or 1
     E = len(src)
-    probe = min(E, 20_000)
-    a = max(0, E // 2 - probe // 2)
-    t0 = time.perf_counter()
-    oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=(a, a + probe), threads=threads)
-    per_root = (time.perf_counter() - t0) / max(probe, 1)
-    if per_root * E <= budget_s:
-        rng, sample = (0, E), "full workload (all %d roots, all %d motifs, mined independently)" % (E, len(cfg.motifs))
-    else:
-        n = max(1000, int(budget_s / max(per_root, 1e-12)))
-        a = max(0, E // 2 - n // 2)
-        rng = (a, min(E, a + n))
-        sample = "contiguous root range [%d, %d) of %d (%.1f%%), all %d motifs" % (
-            rng[0], rng[1], E, 100.0 * (rng[1] - rng[0]) / E, len(cfg.motifs))
-    reps, elapsed, counts = 0, 0.0, None
+    ranges = plan_sample(oracle, cfg, src, dst, t, V, budget_s, n_chunks, threads)
+    reps, elapsed, per = 0, 0.0, None
     while reps < 1 or (elapsed < 3.0 and reps < 5):
         t0 = time.perf_counter()
-        counts = oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=rng, threads=threads)
+        _, per = oracle_on_ranges(oracle, cfg, src, dst, t, V, ranges, threads)
         elapsed += time.perf_counter() - t0
         reps += 1
-    roots = (rng[1] - rng[0]) * reps
+    roots = sum(b - a for a, b in ranges) * reps
     rec = {"value": roots / elapsed, "unit": UNIT, "cores": threads, "kind": "oracle",
-           "sample": sample + ("; %d passes" % reps), "seconds": elapsed / reps}
-    return rec, (counts if rng == (0, E) else None), rng
+           "sample": describe_sample(ranges, E, len(cfg.motifs)) + ("; %d passes" % reps),
+           "seconds": elapsed / reps, "host": cpu_info()}
+    return rec, per, ranges
 
 
 def config_record(cfg, world, flush_mb):
+    """The workload record; both arms (--impl mayura / reference) print exactly this dict."""
+    gb = 96.0 * cfg.n_edges / 1e9  # device graph arrays, ~96 B per edge (DESIGN.md §5)
+    l2 = "flushed between timed steps (%d MiB write)" % flush_mb
+    if gb * 1e9 > 126e6:
+        l2 += "; the graph arrays (~%.1f GB) are also larger than the 126 MB L2" % gb
     return {"workload": "%s: %s" % (cfg.name, cfg.title), "name": cfg.name, "n_vertices": cfg.n_vertices,
             "n_edges": cfg.n_edges, "delta": cfg.delta, "motifs": list(cfg.motifs),
             "generator": "cascade-Zipf alpha=%g p=%g tau=%gs span=%ds seed=%d" % (
                 cfg.alpha, cfg.p, cfg.tau, cfg.span, cfg.seed),
-            "parallelism": "root-partition%d" % world,
-            "l2": "flushed between timed steps (%d MiB write)" % flush_mb}
+            "parallelism": "root-partition%d" % world, "l2": l2}
 
 
 def run_reference(args, cfg, world, rank):
-    """--impl reference: the CPU oracle (the only reference this paper-only tier has)."""
+    """--impl reference: the CPU oracle as it stands (the only reference this paper-only tier
+    has), on the host cores, each step a bounded sample of the same workload: the same evenly
+    spaced root chunks as the cpu_baseline leg, sized so the whole --steps/--warmup run takes
+    ~150 s.  Under torchrun only rank 0 runs and prints; the other ranks exit 0."""
     if rank != 0:
         return
     src, dst, t, V = cfg.graph()
@@ -199,29 +269,23 @@ def run_reference(args, cfg, world, rank):
     oracle.build()
     threads = os.cpu_count() or 1
     E = len(src)
-    probe = min(E, 20_000)
-    a = max(0, E // 2 - probe // 2)
-    t0 = time.perf_counter()
-    oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=(a, a + probe), threads=threads)
-    per_root = (time.perf_counter() - t0) / max(probe, 1)
     step_budget = max(1.0, 150.0 / max(1, args.steps + args.warmup))
-    n = E if per_root * E <= step_budget else max(1000, int(step_budget / max(per_root, 1e-12)))
-    a = max(0, E // 2 - n // 2)
-    rng = (a, min(E, a + n))
+    ranges = plan_sample(oracle, cfg, src, dst, t, V, step_budget, args.cpu_chunks, threads)
     for _ in range(args.warmup):
-        oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=rng, threads=threads)
+        oracle_on_ranges(oracle, cfg, src, dst, t, V, ranges, threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=rng, threads=threads)
+        oracle_on_ranges(oracle, cfg, src, dst, t, V, ranges, threads)
     el = time.perf_counter() - t0
-    value = (rng[1] - rng[0]) * args.steps / el
-    sample = ("full workload" if rng == (0, E) else "root range [%d, %d) of %d" % (rng[0], rng[1], E))
+    n = sum(b - a for a, b in ranges)
+    value = n * args.steps / el
+    sample = describe_sample(ranges, E, len(cfg.motifs)) + " per step; O2 per-motif Algorithm-1 backtracking"
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-           "data": "synthetic", "config": config_record(cfg, 1, 0),
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                            "sample": sample + " per step; O2 per-motif Algorithm-1 backtracking"},
+           "data": "synthetic", "config": config_record(cfg, world, args.flush_mb),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                            "host": cpu_info()},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -387,7 +451,11 @@ def main():
         peak, peak_src = json.load(open(peaks_path))["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs (measured)"
     else:
         peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
-    achieved = st["bytes_alg"] / (ms_kern * 1e-3) / 1e9
+    # SURVEY.md §8(d) B_alg: 16 B per root (src, dst, tr, hi) + 8 B per window entry + one 8-B
+    # terminating entry per window; successor pointers and search probes are reported as overhead
+    n_range = re_ - rb
+    b_alg = 16 * n_range + 8 * (st["entries"] + st["windows"])
+    achieved = b_alg / (ms_kern * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -399,9 +467,17 @@ def main():
                 "traffic": traffic,
                 "kernel": KERNELS.get(form, form), "kernel_form": form,
                 "kernel_ms": ms_kern,
-                "window_end_kernel_ms": ms_win, "bytes_alg_per_launch": st["bytes_alg"],
-                "bytes_alg_per_root": st["bytes_alg"] / max(1, re_ - rb), "peak_source": peak_src,
-                "note": "latency-bound irregular traversal; frac = algorithmic bytes / event-timed duration"}
+                "window_end_kernel_ms": ms_win, "bytes_alg_per_launch": b_alg,
+                "bytes_alg_per_root": b_alg / max(1, n_range),
+                "bytes_alg_formula": "SURVEY.md:540 B_alg = 16*roots + 8*(window entries + windows)",
+                "overhead": {"succ_ptr_bytes": 16 * st["nodes"], "search_probe_bytes_S_alg": 4 * st["probes"],
+                             "impl_bytes_r1": st["bytes_alg"],
+                             "note": "successor pointers (16 B per expanded node incl. the root), window-search "
+                                     "probes (SURVEY.md:542 S_alg) and the r1 implementation count; frontier "
+                                     "records / task stacks show in traffic"},
+                "peak_source": peak_src,
+                "note": "latency-bound irregular traversal; frac = algorithmic bytes / event-timed duration of "
+                        "the co-mining pass (all its kernels)"}
 
     # e2e through the public C ABI from host buffers
     e2e = None
@@ -444,15 +520,13 @@ def main():
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         unbind_all_cores()  # the oracle baseline uses every host core
-        cpu, ocounts, orng = cpu_baseline(cfg, src, dst, t, V, args.cpu_budget_s)
-        if ocounts is not None:
-            parity = "exact" if ocounts == got else "MISMATCH"
-        else:
-            sub = torch.zeros(k, dtype=torch.int64, device=dev)
-            import oracle
-            ocounts = oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=orng)
-            M.mayura_comine(g.handle, tree.handle, orng[0], orng[1], sp, sub)
-            parity = "exact on sampled root range" if sub.cpu().tolist() == ocounts else "MISMATCH"
+        cpu, per, ranges = cpu_baseline(cfg, src, dst, t, V, args.cpu_budget_s, args.cpu_chunks)
+        if ranges == [(0, E)]:
+            parity = "exact" if per[0] == got else "MISMATCH"
+        else:  # every sampled chunk, per motif, vs the GPU on the same root range
+            bad = [i for i, ((a, b), oc) in enumerate(zip(ranges, per)) if M.comine(g, tree, (a, b)) != oc]
+            parity = ("exact on all %d sampled chunks" % len(ranges)) if not bad else \
+                     "MISMATCH on chunks %s" % bad[:8]
 
     if rank == 0:
         out = {"metric": METRIC, "value": E / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,

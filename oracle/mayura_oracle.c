@@ -144,7 +144,9 @@ static void o1_rec(o1_ctx *c, uint32_t j) {
     if (j == c->m) { c->count += (uint64_t)o1_structure_ok(c); return; }
     const og_graph *g = c->g;
     for (uint64_t e = c->tup[j - 1] + 1; e < g->E; e++) {
-        if (g->t[e] - g->t[c->tup[0]] > c->delta) break;    /* window: t_m - t_1 <= delta */
+        /* window: t_m - t_1 <= delta; t_m >= t_1 here, so the difference is exact
+         * in u64 for any int64 timestamps (a signed subtraction overflows for t_1 < 0 < t_m) */
+        if ((uint64_t)g->t[e] - (uint64_t)g->t[c->tup[0]] > (uint64_t)c->delta) break;
         if (!(g->t[e] > g->t[c->tup[j - 1]])) continue;     /* strict order t_{j-1} < t_j */
         c->tup[j] = e;
         o1_rec(c, j + 1);
@@ -230,7 +232,10 @@ static void o2_match_edge(o2_ctx *c, uint32_t eM) {
     uint32_t uM = c->mu[eM], vM = c->mv[eM];
     int64_t uG = c->m2g[uM];                                 /* line 205 */
     int64_t t_prev = g->t[c->e_stack[c->top - 1]];
-    int64_t t_last = g->t[c->e_stack[0]] + c->delta;         /* window end (R2), overflow-free for test ranges */
+    /* window end t_1 + delta (R2, PAPER.md:125 t_m - t_1 <= delta), saturated at INT64_MAX: delta >= 0,
+     * so "t_1 > INT64_MAX - delta" is the overflow test and itself cannot overflow */
+    int64_t t_root = g->t[c->e_stack[0]];
+    int64_t t_last = t_root > INT64_MAX - c->delta ? INT64_MAX : t_root + c->delta;
     if (uG != -1) {                                          /* cands = N(u_G) */
         const uint64_t *ids = g->out_eid;
         uint64_t lo = g->out_off[uG], hi = g->out_off[uG + 1];

@@ -92,6 +92,10 @@ constexpr uint32_t kChunk = 8;     // output slots a thread reserves at once (ex
 constexpr uint32_t kHole = 0xFFFFu; // node id of an unused reserved slot (skipped by readers)
 
 __device__ __forceinline__ void count_add(Ctx &c, uint32_t slot, uint32_t n) {
+    if (!c.cnt) {  // groups with many completion slots: block-shared u64 counters (thread_cnt)
+        atomicAdd(&c.tot[slot], (unsigned long long)n);
+        return;
+    }
     uint32_t *q = c.cnt + slot * c.stride;
     uint32_t v = *q + n;
     if (v >= 0x80000000u) {
@@ -411,17 +415,26 @@ __device__ __forceinline__ bool load_root(const BParams &p, uint32_t r, PM<MAXV>
     return true;
 }
 
-// shared memory: nodes | groups | slot totals | per-thread u32 counters | stripe prefix
+// Per-thread u32 counters (one per completion slot) while they take <= kThreadCntSmem bytes of
+// shared memory; groups with more completion slots (e.g. the 1,657-motif 4-edge family) count
+// with shared-memory u64 atomics on the block totals instead, so any group within the ABI
+// limits launches (the node and group tables alone stay under 120 KB).
+constexpr size_t kThreadCntSmem = 64 * 1024;
+__host__ __device__ inline bool thread_cnt(uint32_t ns, int threads) {
+    return (size_t)ns * threads * 4 <= kThreadCntSmem;
+}
+// shared memory: nodes | groups | slot totals | per-thread u32 counters (thread_cnt) | stripe prefix
 __host__ __device__ inline size_t smem_bytes(uint32_t nn, uint32_t ng, uint32_t ns, int threads) {
     return lane::align16((size_t)nn * sizeof(lane::LNode)) + lane::align16((size_t)ng * sizeof(DGroup)) +
-           lane::align16((size_t)ns * 8) + (size_t)ns * threads * 4 + (kStripes + 1) * 4;
+           lane::align16((size_t)ns * 8) + (thread_cnt(ns, threads) ? (size_t)ns * threads * 4 : 0) +
+           (kStripes + 1) * 4;
 }
 
 struct Smem {
     lane::LNode *nodes;
     DGroup *groups;
     unsigned long long *tot;
-    uint32_t *cnt;
+    uint32_t *cnt;      // per-thread counters, or null (!thread_cnt: atomics on tot)
     uint32_t *pref;
 };
 
@@ -434,13 +447,15 @@ __device__ __forceinline__ Smem smem_setup(const BParams &p, unsigned char *smem
     o += lane::align16((size_t)p.n_groups * sizeof(DGroup));
     s.tot = reinterpret_cast<unsigned long long *>(smem + o);
     o += lane::align16((size_t)p.n_slots * 8);
-    s.cnt = reinterpret_cast<uint32_t *>(smem + o);
-    o += (size_t)p.n_slots * blockDim.x * 4;
+    const bool tc = thread_cnt(p.n_slots, blockDim.x);
+    s.cnt = tc ? reinterpret_cast<uint32_t *>(smem + o) : nullptr;
+    o += tc ? (size_t)p.n_slots * blockDim.x * 4 : 0;
     s.pref = reinterpret_cast<uint32_t *>(smem + o);
     for (uint32_t i = threadIdx.x; i < p.n_nodes; i += blockDim.x) s.nodes[i] = p.nodes[i];
     for (uint32_t i = threadIdx.x; i < p.n_groups; i += blockDim.x) s.groups[i] = p.groups[i];
     for (uint32_t i = threadIdx.x; i < p.n_slots; i += blockDim.x) s.tot[i] = 0;
-    for (uint32_t i = 0; i < p.n_slots; i++) s.cnt[i * blockDim.x + threadIdx.x] = 0;
+    if (tc)
+        for (uint32_t i = 0; i < p.n_slots; i++) s.cnt[i * blockDim.x + threadIdx.x] = 0;
     if (!level0 && threadIdx.x == 0) {
         uint32_t acc = 0;
         for (int i = 0; i < kStripes; i++) {
@@ -457,7 +472,7 @@ template <bool STATS>
 __device__ __forceinline__ void flush(const BParams &p, const Smem &s, Ctx &c) {
     __syncthreads();
     const int lane_id = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (uint32_t sl = threadIdx.x >> 5; sl < p.n_slots; sl += nw) {
+    for (uint32_t sl = threadIdx.x >> 5; s.cnt && sl < p.n_slots; sl += nw) {
         unsigned long long v = 0;
         for (uint32_t i = lane_id; i < blockDim.x; i += 32) v += s.cnt[sl * blockDim.x + i];
 #pragma unroll
@@ -487,7 +502,7 @@ __global__ void __launch_bounds__(kTB) expand_kernel(const __grid_constant__ BPa
     extern __shared__ __align__(16) unsigned char smem[];
     const Smem s = smem_setup(p, smem, LEVEL0);
     Ctx c;
-    c.cnt = s.cnt + threadIdx.x;
+    c.cnt = s.cnt ? s.cnt + threadIdx.x : nullptr;
     c.stride = blockDim.x;
     c.tot = s.tot;
 #pragma unroll
@@ -632,7 +647,7 @@ __global__ void __launch_bounds__(kTB) long_kernel(const __grid_constant__ BPara
     extern __shared__ __align__(16) unsigned char smem[];
     const Smem s = smem_setup(p, smem, LEVEL0);
     Ctx c;
-    c.cnt = s.cnt + threadIdx.x;
+    c.cnt = s.cnt ? s.cnt + threadIdx.x : nullptr;
     c.stride = blockDim.x;
     c.tot = s.tot;
 #pragma unroll

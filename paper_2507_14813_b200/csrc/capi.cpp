@@ -160,7 +160,7 @@ extern "C" mayura_status mayura_partition_roots(mayura_graph g, int64_t delta, u
         std::vector<uint64_t> pref(E + 1, 0);
         uint64_t k = 0;  // first index with t > t_r + delta
         for (uint64_t r = 0; r < E; r++) {
-            const int64_t lim = (delta > INT64_MAX - t[r]) ? INT64_MAX : t[r] + delta;
+            const int64_t lim = (t[r] > INT64_MAX - delta) ? INT64_MAX : t[r] + delta;  // delta >= 0: no overflow
             if (k < r + 1) k = r + 1;
             while (k < E && t[k] <= lim) k++;
             pref[r + 1] = pref[r] + proxy_host(g, r, (uint32_t)(k - 1));

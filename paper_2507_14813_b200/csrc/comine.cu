@@ -50,7 +50,7 @@ __device__ __forceinline__ void pdl_begin() {
 // short) then binary search
 __device__ __forceinline__ uint32_t window_end_of(const int64_t *__restrict__ T, uint32_t E, int64_t delta, uint32_t r) {
     const int64_t x = __ldg(T + r);
-    const int64_t lim = (delta > INT64_MAX - x) ? INT64_MAX : x + delta;
+    const int64_t lim = (x > INT64_MAX - delta) ? INT64_MAX : x + delta;  // delta >= 0: no overflow
     uint32_t a = r + 1, step = 1;  // invariant: T[a-1] <= lim
     uint32_t b = E;
     while (a < E) {
@@ -172,29 +172,47 @@ mayura_status cuda_fail(cudaError_t e, const char *what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, what); \
     } while (0)
 
+// Resident blocks per SM of kernel `kern` at `block` threads and `smem` dynamic bytes, with the
+// opt-in shared-memory attribute set -- both driver calls made once per (kernel, device, smem)
+// and cached: a C2 query issues 6 launches, and the per-launch attribute + occupancy queries
+// were ~12 driver calls of host overhead on the end-to-end path.
+struct OccKey {
+    const void *kern;
+    int dev;
+    size_t smem;
+};
+cudaError_t blocks_per_sm(const void *kern, int block, size_t smem, int *per_sm) {
+    static std::mutex mu;
+    static std::vector<std::pair<OccKey, int>> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (const auto &e : cache)
+            if (e.first.kern == kern && e.first.dev == dev && e.first.smem == smem) {
+                *per_sm = e.second;
+                return cudaSuccess;
+            }
+    }
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int n = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, block, smem);
+    if (e != cudaSuccess) return e;
+    if (n < 1) n = 1;
+    std::lock_guard<std::mutex> lk(mu);
+    cache.push_back({OccKey{kern, dev, smem}, n});
+    *per_sm = n;
+    return cudaSuccess;
+}
+
 template <int MAXV, bool LANECNT, bool STATS, bool GEN, bool ENUM = false>
 cudaError_t launch_lane_t(const lane::LParams &p, size_t smem, cudaStream_t s, int sms, uint32_t *grid_out = nullptr) {
     auto kern = lane::comine_lane_kernel<MAXV, LANECNT, STATS, GEN, ENUM>;
-    static std::mutex mu;
-    static size_t cached_smem = 0;
-    static int cached_dev = -1, cached_per_sm = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
     int per_sm = 0;
     {
-        std::lock_guard<std::mutex> lk(mu);
-        if (cached_smem == smem && cached_dev == dev) per_sm = cached_per_sm;
-    }
-    if (per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = blocks_per_sm((const void *)kern, lane::kLB, smem, &per_sm);
         if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, lane::kLB, smem);
-        if (e != cudaSuccess) return e;
-        if (per_sm < 1) per_sm = 1;
-        std::lock_guard<std::mutex> lk(mu);
-        cached_smem = smem;
-        cached_dev = dev;
-        cached_per_sm = per_sm;
     }
     uint32_t grid = (uint32_t)(sms * per_sm);
     const uint32_t need = (p.n_roots + lane::kLB - 1) / lane::kLB;
@@ -322,10 +340,8 @@ template <int MAXV, bool L0, bool STATS>
 cudaError_t launch_bfs_pass(const bfs::BParams &p, bool long_pass, cudaStream_t s, int sms) {
     auto kern = long_pass ? bfs::long_kernel<MAXV, L0, STATS> : bfs::expand_kernel<MAXV, L0, STATS>;
     const size_t smem = bfs::smem_bytes(p.n_nodes, p.n_groups, p.n_slots, bfs::kTB);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bfs::kTB, smem);
+    cudaError_t e = blocks_per_sm((const void *)kern, bfs::kTB, smem, &per_sm);
     if (e != cudaSuccess) return e;
     uint32_t grid = (uint32_t)(sms * (per_sm > 0 ? per_sm : 1));
     if (L0 && !long_pass) {
@@ -372,10 +388,8 @@ cudaError_t launch_flat_level(const flat::FParams &f, cudaStream_t s, int sms) {
     const size_t smem = bfs::smem_bytes(f.b.n_nodes, f.b.n_groups, f.b.n_slots, flat::kTB);
     for (int pass = 0; pass < 2; pass++) {
         auto kern = pass == 0 ? flat::flat_win_kernel<MAXV, L0> : flat::flat_entry_kernel<MAXV, L0>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
         int per_sm = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, flat::kTB, smem);
+        cudaError_t e = blocks_per_sm((const void *)kern, flat::kTB, smem, &per_sm);
         if (e != cudaSuccess) return e;
         uint32_t grid = (uint32_t)(sms * (per_sm > 0 ? per_sm : 1));
         if (L0 && pass == 0) grid = std::max(1u, std::min(grid, (f.b.n_roots + flat::kTB - 1) / flat::kTB));
@@ -424,6 +438,10 @@ mayura_status ensure_bfs_buffers(mayura_graph_s *g, uint32_t words, int nbufs) {
         // keep the old size only when the buffer count is unchanged (two buffers of a size
         // budgeted for one would take 80 % of the device)
         const size_t want = g->bfs_nbufs >= nbufs ? std::max(bytes, g->bfs_bytes) : bytes;
+        // queries already enqueued on any stream (e.g. enqueue-only calls with counts_on_device
+        // = 1 on a non-blocking stream) may still read the old buffers: dfree orders on the
+        // legacy stream only, so drain the device before the memory returns to the pool
+        if (g->d_bfs[0] || g->d_bfs[1]) cudaDeviceSynchronize();
         for (int i = 0; i < 2; i++)
             if (g->d_bfs[i]) dfree(g->d_bfs[i]), g->d_bfs[i] = nullptr;
         g->device_bytes -= g->bfs_nbufs * g->bfs_bytes;
@@ -744,7 +762,7 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
     unsigned long long *d_counts = reinterpret_cast<unsigned long long *>(counts_out);
     if (!on_device || stats_host) {
         if (g->d_counts_cap < k) {
-            if (g->d_counts) dfree(g->d_counts);
+            if (g->d_counts) cudaDeviceSynchronize(), dfree(g->d_counts);  // may be in flight (see above)
             g->d_counts = nullptr;
             g->d_counts_cap = 0;
             CK((cudaError_t)dmalloc((void **)&g->d_counts, sizeof(unsigned long long) * k), "cudaMalloc(counts)");
@@ -858,10 +876,8 @@ cudaError_t launch_flat_enum_v(flat::EParams e, uint32_t levels, uint32_t *bufs[
     const size_t smem = bfs::smem_bytes(e.b.n_nodes, e.b.n_groups, e.b.n_slots, flat::kTB);
     e.win_seg_cap = win_cap / bfs::kStripes;
     auto launch = [&](auto kern, bool roots) -> cudaError_t {
-        cudaError_t er = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (er != cudaSuccess) return er;
         int per_sm = 0;
-        er = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, flat::kTB, smem);
+        cudaError_t er = blocks_per_sm((const void *)kern, flat::kTB, smem, &per_sm);
         if (er != cudaSuccess) return er;
         uint32_t grid = (uint32_t)(sms * (per_sm > 0 ? per_sm : 1));
         if (roots) grid = std::max(1u, std::min(grid, (e.b.n_roots + flat::kTB - 1) / flat::kTB));
@@ -1039,7 +1055,7 @@ mayura_status run_enum(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint6
                  b_sl = lane::align16(4 * (size_t)std::max(ns, 1u)), b_lb = 4 * LB_N * 4;
     const size_t need_b = lane::align16(b_counts) + 2 * b_w + b_sw + b_sl + b_lb + scan_bytes + 256;
     if (g->enum_bytes < need_b) {
-        if (g->d_enum) dfree(g->d_enum);
+        if (g->d_enum) cudaDeviceSynchronize(), dfree(g->d_enum);  // may be in flight
         g->d_enum = nullptr;
         g->enum_bytes = 0;
         CK((cudaError_t)dmalloc((void **)&g->d_enum, need_b), "cudaMalloc(enumeration scratch)");

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kTB) flat_win_kernel(const __grid_constant__ F
     const bfs::BParams &p = f.b;
     const bfs::Smem s = bfs::smem_setup(p, smem, L0);
     bfs::Ctx c;
-    c.cnt = s.cnt + threadIdx.x;
+    c.cnt = s.cnt ? s.cnt + threadIdx.x : nullptr;
     c.stride = blockDim.x;
     c.tot = s.tot;
 #pragma unroll
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kTB) flat_entry_kernel(const __grid_constant__
     const bfs::BParams &p = f.b;
     const bfs::Smem s = bfs::smem_setup(p, smem, L0);
     bfs::Ctx c;
-    c.cnt = s.cnt + threadIdx.x;
+    c.cnt = s.cnt ? s.cnt + threadIdx.x : nullptr;
     c.stride = blockDim.x;
     c.tot = s.tot;
 #pragma unroll

@@ -151,7 +151,7 @@ __global__ void k_proxy(const int64_t *t, uint32_t E, int64_t delta, const uint3
                         const uint2 *in_ent, unsigned long long *proxy) {
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < E; r += gridDim.x * blockDim.x) {
         const int64_t x = t[r];
-        const int64_t lim = (delta > INT64_MAX - x) ? INT64_MAX : x + delta;
+        const int64_t lim = (x > INT64_MAX - delta) ? INT64_MAX : x + delta;  // delta >= 0: no overflow
         uint32_t a = r + 1, step = 1, b = E;  // first index with t > lim, galloping from r
         while (a < E) {
             const uint32_t probe = min(E - 1, a + step - 1);

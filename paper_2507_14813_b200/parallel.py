@@ -38,7 +38,9 @@ def reduce_counts(counts, group=None):
 def comine_distributed(graph: Graph, tree: MGTree, counts_out, stream: Optional[int] = None,
                        group=None, rank: Optional[int] = None, world: Optional[int] = None):
     """Co-mine this rank's share of the roots into the device tensor ``counts_out``
-    (k int64 on the graph's GPU), then all-reduce it.  Returns ``counts_out``, which
+    (k int64 on the graph's GPU), then all-reduce it.  ``stream`` (a cudaStream_t as int)
+    defaults to torch's current stream on the tensor's device; a different stream is joined
+    to the current one with an event before the collective.  Returns ``counts_out``, which
     holds the whole-graph counts on every rank once the stream completes."""
     import torch.distributed as dist
     if rank is None or world is None:
@@ -47,7 +49,18 @@ def comine_distributed(graph: Graph, tree: MGTree, counts_out, stream: Optional[
         else:
             rank, world = 0, 1
     rb, re_ = shard_range(graph, tree.delta, rank, world)
+    import torch
+    dev = counts_out.device if getattr(counts_out, "is_cuda", False) else None
+    cur = torch.cuda.current_stream(dev) if dev is not None else None
+    if stream is None and cur is not None:
+        stream = cur.cuda_stream          # not the legacy default stream: all_reduce follows `cur`
     mayura_comine(graph.handle, tree.handle, rb, re_, stream, counts_out)
+    if cur is not None and stream != cur.cuda_stream:
+        # the collective is ordered after torch's current stream only: make it wait for the
+        # mining kernels enqueued on the caller's stream
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.ExternalStream(stream, device=dev))
+        cur.wait_event(ev)
     return reduce_counts(counts_out, group)
 
 

@@ -315,7 +315,16 @@ class Config:
     n_bursts: int = 0
     planted: int = 0          # AML patterns planted on top of the background (C5)
 
-    def graph(self):
+    def graph(self, cache: bool = True):
+        """(src, dst, t, V) in input order.  Workloads of >= 1 M edges go through the versioned
+        binary cache (synth/cache.py): the first process on a machine generates and writes it,
+        the others (N bench ranks, the second bench arm, later test modules) load it."""
+        if cache and self.n_edges >= 1_000_000:
+            from . import cache as _cache
+            return _cache.cached(self)
+        return self.generate()
+
+    def generate(self):
         if not self.planted:
             return cascade_zipf(self.n_vertices, self.n_edges, self.span, self.alpha, self.p,
                                 self.tau, self.seed, self.burst_frac, self.burst_width,

@@ -196,3 +196,22 @@ def test_kernel_form_host_only_graph(M):
     assert M.mayura_kernel_form(None) == "none"
     assert M.mayura_enum_form(g.handle) == "none"
     assert M.mayura_enum_form(None) == "none"
+
+
+def test_partition_roots_shifted_timestamps(M):
+    """The window end t_r + delta saturates instead of wrapping: a partition of
+    timestamps shifted to negative values equals the numpy rule on the shifted graph and the
+    partition of the unshifted graph (it depends on differences only)."""
+    src, dst, t, V = synth.random_graph(3, 30, 3000, 5000)
+    g0 = M.Graph(src, dst, t, V, device=-1)
+    for shift in (-(1 << 40), -(1 << 62)):
+        g = M.Graph(src, dst, t + np.int64(shift), V, device=-1)
+        ex = g.export()
+        for parts in (2, 4):
+            ref, _ = _partition_reference(ex, 600, parts)
+            assert g.partition(600, parts) == ref == g0.partition(600, parts)
+    # timestamps next to INT64_MAX with a huge delta: every later edge is in every window
+    top = np.iinfo(np.int64).max - 5000 + t
+    g = M.Graph(src, dst, top, V, device=-1)
+    big = g.partition(np.iinfo(np.int64).max, 4)
+    assert big[0] == 0 and big[-1] == 3000 and all(a <= b for a, b in zip(big, big[1:]))

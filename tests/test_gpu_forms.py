@@ -79,8 +79,11 @@ def test_form_edge_cases(M, oracle_mod):
     src, dst, t, V = synth.random_graph(9, 10, 500, 100)
     g2 = synth.group(synth.GROUP_C2)
     assert run(M, src, dst, t, V, g2, 0) == oracle_mod.backtrack(src, dst, t, V, g2, 0)
-    big = 2 ** 62
-    assert run(M, [0, 1], [1, 0], [big, big + 5], 2, [synth.MOTIFS["recip2"]], 2 ** 62) == [1]
+    big = 2 ** 62   # t_r + delta = 2^63 would wrap: compared with the (saturating) oracle
+    rm = [synth.MOTIFS["recip2"]]
+    assert run(M, [0, 1], [1, 0], [big, big + 5], 2, rm, 2 ** 62) == \
+        oracle_mod.backtrack([0, 1], [1, 0], [big, big + 5], 2, rm, 2 ** 62) == \
+        [oracle_mod.python_bruteforce([0, 1], [1, 0], [big, big + 5], rm[0], 2 ** 62)]
     assert run(M, src, dst, t, V, [synth.MOTIFS["edge1"]], 10) == \
         oracle_mod.backtrack(src, dst, t, V, [synth.MOTIFS["edge1"]], 10)
 
@@ -105,3 +108,17 @@ def test_form_maximum_motif_size(M, oracle_mod):
     src, dst, t, V = synth.random_graph(32, 40, 60, 30, 0.0)
     disj = [[(2 * i, 2 * i + 1) for i in range(8)]]
     assert run(M, src, dst, t, V, disj, 9) == oracle_mod.backtrack(src, dst, t, V, disj, 9)
+
+
+def test_form_family_m4(M, oracle_mod):
+    """The full 4-edge family: 1,657 canonical motifs, 1,752 trie rows -- more completion slots
+    than per-thread shared-memory counters can hold, so the breadth-first / flat passes count
+    with block-shared atomics (bfs::thread_cnt).  Exact vs the oracle, and the family identity
+    (P4: the sum over the family = all increasing windowed 4-tuples of non-self-loop edges)."""
+    from tests import _pins
+    fam = _pins.canonical_motifs(4)
+    assert len(fam) == 1657
+    src, dst, t, V = synth.random_graph(23, 7, 220, 90, 0.03)
+    got = run(M, src, dst, t, V, fam, 30)
+    assert got == oracle_mod.backtrack(src, dst, t, V, fam, 30)
+    assert sum(got) == _pins.family_total(src, dst, t, 4, 30)

@@ -154,8 +154,11 @@ def test_edge_cases(M, oracle_mod):
     src, dst, t, V = synth.random_graph(9, 10, 500, 100)
     assert gpu_counts(M, src, dst, t, V, synth.group(synth.GROUP_C2), 0) == \
         oracle_mod.backtrack(src, dst, t, V, synth.group(synth.GROUP_C2), 0)   # delta = 0
-    big = 2 ** 62
-    assert gpu_counts(M, [0, 1], [1, 0], [big, big + 5], 2, [synth.MOTIFS["recip2"]], 2 ** 62) == [1]
+    big = 2 ** 62   # t_r + delta = 2^63 would wrap: compared with the (saturating) oracle
+    rm = [synth.MOTIFS["recip2"]]
+    assert gpu_counts(M, [0, 1], [1, 0], [big, big + 5], 2, rm, 2 ** 62) == \
+        oracle_mod.backtrack([0, 1], [1, 0], [big, big + 5], 2, rm, 2 ** 62) == \
+        [oracle_mod.python_bruteforce([0, 1], [1, 0], [big, big + 5], rm[0], 2 ** 62)]
 
 
 def test_disconnected_prefix_motifs(M, oracle_mod):

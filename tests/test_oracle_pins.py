@@ -233,3 +233,54 @@ def test_c5s_planted_lower_bounds(oracle_mod):
     got = dict(zip(cfg.motifs, oracle_mod.backtrack(src, dst, t, V, cfg.group(), cfg.delta)))
     for name, lb in _planted_lower_bounds(planted).items():
         assert got[name] >= lb, name
+
+
+# ---------------------------------------------------------------- int64 extremes
+I64 = np.iinfo(np.int64)
+
+
+def _extreme_cases():
+    """(edges, motif, delta, expected) at the ends of the int64 timestamp domain.  Expected
+    values follow from the definition t_m - t_1 <= delta computed with Python's
+    exact integers (python_bruteforce), so neither t_1 + delta nor t_m - t_1 may wrap."""
+    big = 2 ** 62
+    recip = [(0, 1), (1, 0)]
+    return [
+        ([(0, 1, big), (1, 0, big + 5)], recip, big, 1),                  # t_1 + delta = 2^63 (wraps)
+        ([(0, 1, 5), (1, 0, 9)], recip, I64.max, 1),                       # delta = INT64_MAX
+        ([(0, 1, -big), (1, 0, big - 1)], recip, I64.max, 1),              # t_m - t_1 = 2^63 - 1
+        ([(0, 1, -big), (1, 0, big)], recip, I64.max, 0),                  # t_m - t_1 = 2^63 > delta
+        ([(0, 1, I64.min), (1, 0, I64.max)], recip, I64.max, 0),           # span 2^64 - 1
+        ([(0, 1, I64.min), (1, 0, -1)], recip, I64.max, 1),                # span 2^63 - 1
+        ([(0, 1, -7), (1, 2, -3), (2, 0, -1)], [(0, 1), (1, 2), (2, 0)], 6, 1),   # negative times
+        ([(0, 1, -7), (1, 2, -3), (2, 0, -1)], [(0, 1), (1, 2), (2, 0)], 5, 0),
+        ([(0, 1, I64.max - 2), (1, 2, I64.max - 1), (2, 0, I64.max)], [(0, 1), (1, 2), (2, 0)], 2, 1),
+    ]
+
+
+@pytest.mark.parametrize("case", range(9))
+def test_int64_extremes(oracle_mod, case):
+    edges, motif, delta, exp = _extreme_cases()[case]
+    e = np.array(edges, dtype=object)
+    src = np.array([x[0] for x in edges], np.uint32)
+    dst = np.array([x[1] for x in edges], np.uint32)
+    t = np.array([x[2] for x in edges], np.int64)
+    V = int(max(src.max(), dst.max())) + 1
+    assert oracle_mod.python_bruteforce(src, dst, t, motif, delta) == exp
+    assert oracle_mod.bruteforce(src, dst, t, V, motif, delta) == exp
+    assert oracle_mod.backtrack(src, dst, t, V, [motif], delta, threads=1) == [exp]
+    del e
+
+
+def test_time_translation_invariance(oracle_mod):
+    """P5: counts depend on timestamp differences only, so shifting every
+    timestamp by a constant -- to negative times, or next to INT64_MAX -- changes nothing."""
+    motifs = synth.group(synth.GROUP_C2)
+    for seed in range(12):
+        src, dst, t, V = synth.random_graph(5100 + seed, 9, 120, 60)
+        delta = 3 + seed % 9
+        base = oracle_mod.backtrack(src, dst, t, V, motifs, delta)
+        for shift in (-(1 << 40), -(1 << 62), (1 << 62), int(I64.max) - 60):
+            ts = t + np.int64(shift)
+            assert oracle_mod.backtrack(src, dst, ts, V, motifs, delta) == base, (seed, shift)
+        assert [oracle_mod.bruteforce(src, dst, t - np.int64(1 << 62), V, mo, delta) for mo in motifs[:4]] == base[:4]

@@ -74,6 +74,7 @@ __device__ __forceinline__ uint32_t window_end_of(const int64_t *__restrict__ T,
 #include "bfs.cuh"
 #include "flat.cuh"
 #include "flat_enum.cuh"
+#include "wdfs.cuh"
 
 // a2: hi[r] = (last edge id e with t[e] <= t[r] + delta), by galloping from r (windows
 // are short) then binary search.  Also zeroes the load-balancer words and the output
@@ -123,6 +124,7 @@ struct DeviceTable {
     lane::LNode *lnodes;
     uint32_t *gwant;
     uint32_t n_nodes, n_groups, n_motifs, max_vertices, max_edges, n_slots;
+    uint32_t max_groups;  // anchor groups of the widest node
     bool generic;  // some anchor group searches its list or scans the edge array
 };
 
@@ -194,7 +196,15 @@ cudaError_t blocks_per_sm(const void *kern, int block, size_t smem, int *per_sm)
                 return cudaSuccess;
             }
     }
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the attribute is a per-(kernel, device) maximum: never lower it below a size another
+    // cached entry launches with
+    size_t mx = smem;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (const auto &e : cache)
+            if (e.first.kern == kern && e.first.dev == dev) mx = std::max(mx, e.first.smem);
+    }
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     if (e != cudaSuccess) return e;
     int n = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, block, smem);
@@ -276,6 +286,58 @@ cudaError_t launch_enum(const lane::LParams &p, uint32_t max_vertices, bool gene
     return launch_enum_v<16>(p, generic, s, sms, grid);
 }
 
+// ---- warp-synchronous depth-first kernel (wdfs.cuh)
+// pieces per warp stack: MAYURA_WDFS_CAP overrides (test hook / tuning), else 128; at least one
+// item's worth of pieces (max_groups)
+uint32_t wdfs_cap(uint32_t max_groups) {  // read per call: tests switch it within one process
+    const char *e = getenv("MAYURA_WDFS_CAP");
+    const int v = e ? std::max(1, atoi(e)) : 128;
+    return std::max<uint32_t>((uint32_t)v, max_groups);
+}
+
+template <int MAXV, bool GEN>
+cudaError_t launch_wdfs_t(const wdfs::WParams &w, size_t smem, cudaStream_t s, int sms) {
+    auto kern = wdfs::wdfs_kernel<MAXV, GEN>;
+    int per_sm = 0;
+    cudaError_t e = blocks_per_sm((const void *)kern, wdfs::kWB, smem, &per_sm);
+    if (e != cudaSuccess) return e;
+    cudaError_t le = launch_pdl(kern, (uint32_t)(sms * per_sm), wdfs::kWB, smem, s, w);
+    count_launch();
+    return le != cudaSuccess ? le : cudaGetLastError();
+}
+
+template <int MAXV>
+cudaError_t launch_wdfs_v(wdfs::WParams w, bool generic, cudaStream_t s, int sms) {
+    const bfs::BParams &b = w.b;
+    w.lanecnt = (size_t)b.n_slots * wdfs::kWB * 4 <= kLaneCntSmem ? 1u : 0u;
+    w.o_cnt = (uint32_t)wdfs::off_cnt(b.n_nodes, b.n_groups, b.n_slots);
+    w.o_stk = (uint32_t)wdfs::off_stk(b.n_nodes, b.n_groups, b.n_slots, w.lanecnt != 0);
+    const size_t smem = wdfs::smem_bytes<MAXV>(b.n_nodes, b.n_groups, b.n_slots, w.lanecnt != 0, w.cap);
+    return generic ? launch_wdfs_t<MAXV, true>(w, smem, s, sms) : launch_wdfs_t<MAXV, false>(w, smem, s, sms);
+}
+
+cudaError_t launch_wdfs(const wdfs::WParams &w, uint32_t max_vertices, bool generic, cudaStream_t s, int sms) {
+    if (max_vertices <= 4) return launch_wdfs_v<4>(w, generic, s, sms);
+    if (max_vertices <= 6) return launch_wdfs_v<6>(w, generic, s, sms);
+    if (max_vertices <= 8) return launch_wdfs_v<8>(w, generic, s, sms);
+    return launch_wdfs_v<16>(w, generic, s, sms);
+}
+
+// the warp kernel's stacks fit the block's shared memory (else the lane kernel is used)
+bool wdfs_fits(const DeviceTable &dt) {
+    const uint32_t mv = dt.max_vertices <= 4 ? 4 : dt.max_vertices <= 6 ? 6 : dt.max_vertices <= 8 ? 8 : 16;
+    const bool lc = (size_t)dt.n_slots * wdfs::kWB * 4 <= kLaneCntSmem;
+    const size_t bytes = wdfs::off_stk(dt.n_nodes, dt.n_groups, dt.n_slots, lc) +
+                         (size_t)wdfs::kWarps * (6 + mv) * wdfs_cap(dt.max_groups) * 4;
+    return bytes <= 160 * 1024;
+}
+
+// depth-first phase: MAYURA_DFS=lane selects the lane kernel (A/B), default the warp kernel
+bool use_wdfs() {
+    const char *e = getenv("MAYURA_DFS");
+    return !(e && std::strcmp(e, "lane") == 0);
+}
+
 cudaError_t launch_lane(const lane::LParams &p, uint32_t max_vertices, bool stats, bool generic, cudaStream_t s,
                         int sms) {
     if (max_vertices <= 4) return launch_lane_v<4>(p, stats, generic, s, sms);
@@ -290,7 +352,7 @@ cudaError_t launch_lane(const lane::LParams &p, uint32_t max_vertices, bool stat
 // flat when the graph arrays fit in L2, else hybrid.  Measured (profiles/README.md r04): flat
 // C1 0.172 -> 0.076 ms, C2 0.527 -> 0.321 ms; on DRAM-resident graphs its per-level frontier
 // and window-piece traffic loses (C3 4.9 ms hybrid vs 7.8 ms flat).
-enum KernelKind { K_HYBRID = 0, K_LANE = 1, K_BFS = 2, K_FLAT = 3, K_MIXED = 4 };
+enum KernelKind { K_HYBRID = 0, K_LANE = 1, K_BFS = 2, K_FLAT = 3, K_MIXED = 4, K_WARP = 5 };
 bool l2_resident(const mayura_graph_s *g) {
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
@@ -303,6 +365,7 @@ KernelKind kernel_kind(const mayura_graph_s *g) {  // read per call (tests switc
     if (e && std::strcmp(e, "flat") == 0) return K_FLAT;
     if (e && std::strcmp(e, "hybrid") == 0) return K_HYBRID;
     if (e && std::strcmp(e, "mixed") == 0) return K_MIXED;
+    if (e && std::strcmp(e, "warp") == 0) return K_WARP;
     return l2_resident(g) ? K_FLAT : K_HYBRID;
 }
 // hybrid: a root is split breadth-first only if one of its root-node windows has >= this
@@ -538,7 +601,11 @@ void table_view(const Table &t, uint32_t n_motifs, char *buf, DeviceTable &d) {
     d.max_vertices = t.max_vertices;
     d.max_edges = t.max_edges;
     d.n_slots = 0;
-    for (const DNode &x : t.nodes) d.n_slots += (x.flags & NODE_COMPLETION) ? 1 : 0;
+    d.max_groups = 1;
+    for (const DNode &x : t.nodes) {
+        d.n_slots += (x.flags & NODE_COMPLETION) ? 1 : 0;
+        d.max_groups = std::max<uint32_t>(d.max_groups, (uint32_t)(x.group_end - x.group_begin));
+    }
     d.generic = false;
     for (const DGroup &x : t.groups) d.generic = d.generic || x.kind == ANCHOR_GLOBAL || x.start == START_SEARCH;
 }
@@ -719,6 +786,18 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         CK(launch_lane(q, dt.max_vertices, false, dt.generic, s, sms), "comine_lane_kernel launch");
         return MAYURA_OK;
     }
+    if (kind == K_WARP && !st && wdfs_fits(dt)) {  // the warp kernel straight from the root edges
+        wdfs::WParams w;
+        w.b = bfs_params(g, dt, r0, n_roots, counts, nullptr, 0u);
+        w.b.in.data = nullptr;
+        w.gwant = dt.gwant;
+        w.lb = lb;
+        w.direct = 1;
+        w.cap = wdfs_cap(dt.max_groups);
+        w.max_groups = dt.max_groups;
+        CK(launch_wdfs(w, dt.max_vertices, dt.generic, s, sms), "wdfs_kernel launch");
+        return MAYURA_OK;
+    }
     if (kind == K_FLAT || kind == K_MIXED) levels = std::min(hybrid_levels(), dt.max_edges > 2 ? dt.max_edges - 2 : 0u);
     lane::LParams q = lane_params(g, dt, r0, n_roots, lb, counts, stats, st);
     if (levels > 0) {
@@ -732,6 +811,21 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         uint32_t *bufs[2] = {g->d_bfs[0], g->d_bfs[1]};
         CK(launch_bfs(b, dt.max_vertices, levels, bufs, ctl, g->bfs_seg_cap, st, s, sms), "bfs pass launch");
         if (kind == K_BFS) return MAYURA_OK;
+        if (kind == K_HYBRID && levels == 1 && !st && use_wdfs() && wdfs_fits(dt)) {
+            // depth-first phase in the warp kernel: items = the level's partial matches + light roots
+            wdfs::WParams w;
+            w.b = b;
+            w.b.in.data = bufs[0];
+            w.b.in.cnt = ctl;
+            w.b.in.seg_cap = g->bfs_seg_cap;
+            w.gwant = dt.gwant;
+            w.lb = lb;
+            w.direct = 0;
+            w.cap = wdfs_cap(dt.max_groups);
+            w.max_groups = dt.max_groups;
+            CK(launch_wdfs(w, dt.max_vertices, dt.generic, s, sms), "wdfs_kernel launch");
+            return MAYURA_OK;
+        }
         q.pm = bufs[(levels - 1) & 1];
         q.pm_cnt = ctl + (levels - 1) * kCtlWords;
         q.pm_seg_cap = g->bfs_seg_cap;
@@ -1334,6 +1428,7 @@ extern "C" const char *mayura_kernel_form(mayura_graph g) {
         case K_LANE: return "lane";
         case K_BFS: return "bfs";
         case K_MIXED: return "mixed";
+        case K_WARP: return "warp";
         default: return "hybrid";
     }
 }

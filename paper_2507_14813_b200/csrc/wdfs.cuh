@@ -1,0 +1,387 @@
+// wdfs.cuh -- warp-synchronous depth-first co-mining over a shared-memory stack of window
+// pieces (the default depth-first phase of the hybrid form), included by comine.cu after
+// flat.cuh.
+//
+// Algorithm 3 "Co-Mining" walks, from every root edge, the MG-Tree
+// depth-first: at a node it scans the candidate window of each anchor group (Algo 1
+// l.210-217: entries after the previous edge, up to t_root + delta), tests each candidate
+// (Algo 1 l.219 + full injectivity, reading R4), counts completions (Algo 3 l.661) and
+// descends into inner children (Algo 3 l.665-669).
+//
+// Mapping to a warp.  The depth-first lane kernel (lane.cuh) gives each lane its
+// own search and spends ~10.7 warp instructions per window entry on a divergent per-lane state
+// machine (profiles/r2a_C4.md).  Here the WARP owns one depth-first search frontier, kept as a
+// LIFO stack of window pieces in shared memory; one piece = one anchor-group window of one
+// partial match, with everything needed to test its entries:
+//     { group g, first list position, candidate count n, tr_prev, hi(root), root edge, m2g }
+// Every round the warp takes the top pieces until it has 32 candidate entries (the last piece
+// possibly split) and gives ONE ENTRY TO EACH LANE: an OR-reduction of the pieces' start
+// offsets lets every lane find its piece with one popc/clz; then load, time test, class of the
+// neighbour against the piece's m2g, SIMD child lookup, completion count -- straight-line code
+// on full warps.  A lane whose entry matched an inner child builds the child partial match
+// (its successor pointers were loaded with the entry) and locates the child's windows: start
+// from P / R / search (exact), length bounded by six independent probes at offsets
+// 0, 1, 3, 7, 15, 31 (windows of >= 32 entries: galloping + bisection to a 32-entry bracket);
+// entries past the window fail the time test.  The new pieces are pushed on top (warp-
+// aggregated), so the search stays depth-first and the stack small.  When the stack holds
+// fewer than 32 candidates the warp takes the next 32 items (partial matches written by the
+// breadth-first level, light roots, or root edges) from a global cursor.
+// Stack overflow never loses work: the lane mines that subtree serially (bfs::dfs).
+// Counts are identical to every other kernel form (tests/test_gpu_forms.py).
+
+namespace wdfs {
+
+constexpr int kWB = 128;                 // threads per block
+constexpr int kWarps = kWB / 32;
+
+template <int MAXV>
+struct Piece {
+    // SoA words per piece: 0 group, 1 pos, 2 n, 3 tr_prev, 4 h, 5 root, 6.. m2g[MAXV]
+    static constexpr int F = 6 + MAXV;
+};
+
+struct WParams {
+    bfs::BParams b;          // graph arrays, table, counts, fallback counter; b.in = the breadth-first
+                             // level's partial-match records (hybrid), b.light = its light roots
+    const uint32_t *gwant;   // per group: wants of its first 4 children (bytes, 0xFD pad)
+    uint32_t *lb;            // [0]: item cursor (zeroed per query by the launcher)
+    uint32_t direct;         // 1: the items are the root edges [r0, r0 + n_roots) themselves
+    uint32_t cap;            // pieces per warp stack
+    uint32_t max_groups;     // anchor groups of the widest node
+    uint32_t o_cnt, o_stk;   // dynamic shared memory offsets: lane counters, stacks
+    uint32_t lanecnt;        // 1: per-lane u32 counters; 0: block u64 atomics (many slots)
+};
+
+__host__ __device__ inline size_t off_cnt(uint32_t nn, uint32_t ng, uint32_t ns) {
+    return lane::align16((size_t)nn * sizeof(lane::LNode)) + lane::align16((size_t)ng * sizeof(DGroup)) +
+           lane::align16((size_t)ns * 8);
+}
+__host__ __device__ inline size_t off_stk(uint32_t nn, uint32_t ng, uint32_t ns, bool lanecnt) {
+    return lane::align16(off_cnt(nn, ng, ns) + (lanecnt ? (size_t)ns * kWB * 4 : 0));
+}
+template <int MAXV>
+__host__ __device__ inline size_t smem_bytes(uint32_t nn, uint32_t ng, uint32_t ns, bool lanecnt, uint32_t cap) {
+    return off_stk(nn, ng, ns, lanecnt) + (size_t)kWarps * Piece<MAXV>::F * cap * 4;
+}
+
+// Upper bound of a window's length: entries [lo, lo + n) contain every entry of the window
+// (time rank <= h, before the list's sentinel at `sent`), with at most 31 entries past it.
+__device__ __forceinline__ uint32_t window_len_ub(const uint2 *ent, uint32_t lo, uint32_t sent, uint32_t h) {
+    // six independent loads (lists are padded past their last sentinel, so lo + 31 is in bounds);
+    // an index at or past the sentinel is out of the window whatever it holds
+    const uint32_t o[6] = {0, 1, 3, 7, 15, 31};
+    uint32_t v[6];
+#pragma unroll
+    for (int k = 0; k < 6; k++) v[k] = __ldg(&ent[lo + o[k]].x);
+    uint32_t n = kNone;
+#pragma unroll
+    for (int k = 5; k >= 0; k--)
+        if (lo + o[k] >= sent || v[k] > h) n = o[k];
+    if (n != kNone) return n;
+    // >= 32 entries: gallop (dependent loads, rare), then bisect to a bracket of <= 32
+    uint32_t a = 31, b = 63;
+    for (;;) {
+        if (lo + b >= sent) {
+            b = sent - lo;
+            break;
+        }
+        if (__ldg(&ent[lo + b].x) > h) break;
+        a = b;
+        b = 2 * b + 1;
+    }
+    while (b - a > 32) {
+        const uint32_t m = a + ((b - a) >> 1);
+        if (__ldg(&ent[lo + m].x) <= h) a = m;
+        else b = m;
+    }
+    return b;
+}
+
+// Window of group G for partial match x: first candidate position (exact) and a candidate count
+// covering the window (exact for the all-edges anchor).
+template <int MAXV, bool GEN>
+__device__ __forceinline__ uint32_t window(const bfs::BParams &p, const DGroup &G, const bfs::PM<MAXV> &x,
+                                           uint32_t &n) {
+    if (GEN && G.kind == ANCHOR_GLOBAL) {  // edge ids after tr_prev's tie group, up to hi(root) (R6)
+        uint32_t lo = x.tr_prev, hi2 = x.h + 1;
+        while (lo < hi2) {
+            const uint32_t mid = lo + ((hi2 - lo) >> 1);
+            if (__ldg(p.tr + mid) > x.tr_prev) hi2 = mid;
+            else lo = mid + 1;
+        }
+        n = x.h + 1 > lo ? x.h + 1 - lo : 0;
+        return lo;
+    }
+    const bool out = G.kind == ANCHOR_OUT;
+    const uint2 *ent = out ? p.out_ent : p.in_ent;
+    const uint32_t *off = out ? p.out_off : p.in_off;
+    const uint32_t v = lane::m2g_get<MAXV>(x.m2g, G.anchor);
+    const uint32_t sent = __ldg(off + v + 1) - 1;
+    uint32_t lo;
+    if (G.start < START_R0) {
+        lo = lane::pick4(x.P, G.start);  // exact: successor pointer of the node's own edge
+    } else if (!GEN || G.start < START_SEARCH) {
+        const uint4 R = __ldg(p.eptr + x.root);  // lower bound from the root edge: skip to > tr_prev
+        lo = flat::first_gt(ent, lane::pick4(R, G.start - START_R0), sent, x.tr_prev);
+    } else {  // search the anchor's list for the first entry after tr_prev
+        uint32_t a = __ldg(off + v), b = sent;
+        while (a < b) {
+            const uint32_t mid = a + ((b - a) >> 1);
+            if (__ldg(&ent[mid].x) > x.tr_prev) b = mid;
+            else a = mid + 1;
+        }
+        lo = a;
+    }
+    n = window_len_ub(ent, lo, sent, x.h);
+    return lo;
+}
+
+// Warp-collective: every lane with `has` locates the windows of x's anchor groups and pushes the
+// non-empty ones on the warp's stack (warp-aggregated).  A push past the capacity makes the lane
+// mine x from that group on depth-first itself (exact; counted in p.fallback).
+template <int MAXV, bool GEN>
+__device__ __forceinline__ void open_push(const WParams &w, const lane::LNode *s_nodes, const DGroup *s_groups,
+                                          uint32_t *stk, uint32_t &ps, bool has, const bfs::PM<MAXV> &x,
+                                          bfs::Ctx &c) {
+    const bfs::BParams &p = w.b;
+    const uint32_t lane_id = threadIdx.x & 31, cap = w.cap;
+    uint32_t gb = 0, ng = 0;
+    if (has) {
+        const lane::LNode xn = s_nodes[x.node];
+        gb = xn.group_begin;
+        ng = xn.group_end - xn.group_begin;
+    }
+    const uint32_t mg = __reduce_max_sync(kFull, ng);
+    bool fell = false;
+    for (uint32_t q = 0; q < mg; q++) {
+        uint32_t lo = 0, n = 0;
+        const bool mine = q < ng && !fell;
+        if (mine) lo = window<MAXV, GEN>(p, s_groups[gb + q], x, n);
+        const bool v = mine && n > 0;
+        const unsigned bm = __ballot_sync(kFull, v);
+        const uint32_t slot = ps + __popc(bm & ((1u << lane_id) - 1u));
+        if (v) {
+            if (slot < cap) {
+                stk[0 * cap + slot] = gb + q;
+                stk[1 * cap + slot] = lo;
+                stk[2 * cap + slot] = n;
+                stk[3 * cap + slot] = x.tr_prev;
+                stk[4 * cap + slot] = x.h;
+                stk[5 * cap + slot] = x.root;
+#pragma unroll
+                for (int k = 0; k < MAXV; k++) stk[(6 + k) * cap + slot] = x.m2g[k];
+            } else {
+                atomicAdd(p.fallback, 1u);
+                bfs::dfs<MAXV, false>(p, s_nodes, s_groups, x, c, gb + q);
+                fell = true;
+            }
+        }
+        ps = min(ps + (uint32_t)__popc(bm), cap);
+    }
+    __syncwarp();
+}
+
+template <int MAXV, bool GEN>
+__global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WParams w) {
+    pdl_begin();
+    constexpr int F = Piece<MAXV>::F;
+    const bfs::BParams &p = w.b;
+    extern __shared__ __align__(16) unsigned char smem[];
+    lane::LNode *s_nodes = reinterpret_cast<lane::LNode *>(smem);
+    DGroup *s_groups = reinterpret_cast<DGroup *>(smem + lane::align16((size_t)p.n_nodes * sizeof(lane::LNode)));
+    unsigned long long *s_tot = reinterpret_cast<unsigned long long *>(
+        smem + lane::align16((size_t)p.n_nodes * sizeof(lane::LNode)) + lane::align16((size_t)p.n_groups * sizeof(DGroup)));
+    uint32_t *s_cnt = w.lanecnt ? reinterpret_cast<uint32_t *>(smem + w.o_cnt) : nullptr;
+    const uint32_t tid = threadIdx.x, lane_id = tid & 31, cap = w.cap;
+    uint32_t *stk = reinterpret_cast<uint32_t *>(smem + w.o_stk) + (size_t)(tid >> 5) * F * cap;
+    __shared__ uint32_t s_gw[lane::kGwMax];
+    __shared__ uint32_t s_pref[bfs::kStripes + 1];
+    for (uint32_t i = tid; i < p.n_nodes; i += kWB) s_nodes[i] = p.nodes[i];
+    for (uint32_t i = tid; i < p.n_groups; i += kWB) s_groups[i] = p.groups[i];
+    for (uint32_t i = tid; i < p.n_groups && i < lane::kGwMax; i += kWB) s_gw[i] = w.gwant[i];
+    for (uint32_t i = tid; i < p.n_slots; i += kWB) s_tot[i] = 0;
+    if (s_cnt)
+        for (uint32_t i = 0; i < p.n_slots; i++) s_cnt[i * kWB + tid] = 0;
+    if (tid == 0) {
+        uint32_t acc = 0;
+        for (int i = 0; i < bfs::kStripes; i++) {
+            s_pref[i] = acc;
+            acc += (!w.direct && p.in.data) ? min(p.in.cnt[i], p.in.seg_cap) : 0u;
+        }
+        s_pref[bfs::kStripes] = acc;
+    }
+    __syncthreads();
+
+    bfs::Ctx c;
+    c.cnt = s_cnt ? s_cnt + tid : nullptr;
+    c.stride = kWB;
+    c.tot = s_tot;
+#pragma unroll
+    for (int i = 0; i < ST_N; i++) c.st[i] = 0;
+    c.em_next = c.em_end = 0;
+
+    const lane::LNode root = s_nodes[0];
+    const uint32_t n_pm = s_pref[bfs::kStripes];
+    const uint32_t n_items = w.direct ? p.n_roots : n_pm + (p.light ? *(volatile const uint32_t *)p.light_cnt : 0u);
+
+    uint32_t ps = 0;           // warp-uniform stack height
+    uint32_t cb = 0, cl = 0;   // warp-uniform item chunk
+    bool items_left = true;
+    for (;;) {
+        // ---- the top pieces: candidate counts and their running sum (top first)
+        const uint32_t top = ps;
+        const uint32_t pn = lane_id < top ? stk[2 * cap + top - 1 - lane_id] : 0u;
+        uint32_t incl = pn;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(kFull, incl, o);
+            if (lane_id >= (uint32_t)o) incl += v;
+        }
+        const uint32_t tot = __shfl_sync(kFull, incl, 31);
+
+        bfs::PM<MAXV> x;   // this lane's new partial match: an item, or a child found this round
+        bool has = false;
+        if (tot < 32 && items_left && top + w.max_groups <= cap) {
+            // ---- fewer than 32 candidates stacked: take the next items (one per lane, up to 32, as
+            // many as the stack has room for if each pushes max_groups pieces)
+            if (cl == 0) {
+                uint32_t b = 0, sz = 0;
+                if (lane_id == 0) {
+                    const uint32_t cur = *(volatile uint32_t *)w.lb;
+                    const uint32_t rem = cur < n_items ? n_items - cur : 0u;
+                    sz = max(32u, min(256u, (rem / (4u * gridDim.x * kWarps)) & ~31u));
+                    b = atomicAdd(w.lb, sz);
+                }
+                b = __shfl_sync(kFull, b, 0);
+                sz = __shfl_sync(kFull, sz, 0);
+                if (b >= n_items) {
+                    items_left = false;
+                    continue;
+                }
+                cb = b;
+                cl = min(sz, n_items - b);
+            }
+            const uint32_t take = min(min(32u, cl), (cap - top) / w.max_groups);
+            const uint32_t item = cb + lane_id;
+            cb += take;
+            cl -= take;
+            if (lane_id < take) {
+                if (w.direct) {  // a root edge: count the root node's completion, expand it if inner
+                    const uint32_t r = p.r0 + item;
+                    if (bfs::load_root<MAXV>(p, r, x)) {
+                        if (root.flags & NODE_COMPLETION) bfs::count_add(c, root.slot, 1);
+                        has = (root.flags & NODE_INNER) != 0;
+                    }
+                } else if (item < n_pm) {  // a partial match of the breadth-first level (counted there)
+                    bfs::load_rec<MAXV>(p, s_pref, item, x);
+                    has = x.node != bfs::kHole;
+                } else {  // a light root (its completion was counted by the breadth-first level)
+                    has = bfs::load_root<MAXV>(p, __ldg(p.light + (item - n_pm)), x);
+                }
+            }
+        } else {
+            if (top == 0) break;  // no items left and nothing stacked
+            // ---- this round: T entries, one per lane, from the top pieces (the last one possibly
+            // split).  Throttle: every entry may push up to max_groups pieces; keep them in the stack.
+            const uint32_t room = cap - top;
+            const uint32_t T = min(min(tot, 32u), max(1u, room / max(1u, w.max_groups)));
+            const uint32_t excl = incl - pn;
+            const bool pc = lane_id < top && excl < T;  // this piece contributes entries
+            const uint32_t smask = __reduce_or_sync(kFull, pc ? (1u << excl) : 0u);
+            const uint32_t kf = __popc(__ballot_sync(kFull, lane_id < top && incl <= T));  // taken whole
+            const bool act = lane_id < T;
+            const uint32_t upto = smask & ((2u << lane_id) - 1u);
+            const uint32_t pi = top - 1 - (act ? (uint32_t)__popc(upto) - 1u : 0u);  // this lane's piece
+            const uint32_t at = lane_id - (31 - __clz(upto | 1u));                    // offset in the piece
+            if (act) {
+                const uint32_t g = stk[0 * cap + pi];
+                const uint32_t pos = stk[1 * cap + pi] + at;
+                const uint32_t tp = stk[3 * cap + pi];
+                const uint32_t h = stk[4 * cap + pi];
+                uint32_t m2g[MAXV];
+#pragma unroll
+                for (int k = 0; k < MAXV; k++) m2g[k] = stk[(6 + k) * cap + pi];
+                const DGroup G = s_groups[g];
+                const bool glob = GEN && G.kind == ANCHOR_GLOBAL;
+                uint32_t etr, e1, e2 = 0;
+                uint4 P = make_uint4(0, 0, 0, 0);
+                if (glob) {
+                    etr = __ldg(p.tr + pos);
+                    e1 = __ldg(p.src + pos);
+                    e2 = __ldg(p.dst + pos);
+                    if (G.n_inner) P = __ldg(p.eptr + pos);
+                } else {
+                    const bool out = G.kind == ANCHOR_OUT;
+                    const uint2 e = __ldg((out ? p.out_ent : p.in_ent) + pos);
+                    etr = e.x;
+                    e1 = e.y;
+                    if (G.n_inner) P = __ldg((out ? p.out_ptr : p.in_ptr) + pos);  // with the entry
+                }
+                const bool valid = etr > tp && etr <= h;
+                uint32_t cls;
+                if (glob)
+                    cls = (e1 != e2 && lane::classify<MAXV>(m2g, e1) == CLS_NEW &&
+                           lane::classify<MAXV>(m2g, e2) == CLS_NEW) ? CLS_NEW : 0xFEu;
+                else
+                    cls = lane::classify<MAXV>(m2g, e1);
+                uint32_t hit = kNone;
+                if (G.child_end - G.child_begin <= 4 && g < lane::kGwMax) {
+                    const uint32_t eq = __vcmpeq4(s_gw[g], cls * 0x01010101u);
+                    hit = eq ? G.child_begin + ((__ffs(eq) - 1) >> 3) : kNone;
+                } else {
+                    hit = bfs::find_child(s_nodes, G, cls);
+                }
+                if (valid && hit != kNone) {
+                    const lane::LNode dn = s_nodes[hit];
+                    if (dn.flags & NODE_COMPLETION) bfs::count_add(c, dn.slot, 1);
+                    if (dn.flags & NODE_INNER) {  // the child partial match (Algo 3 l.665-669)
+                        has = true;
+#pragma unroll
+                        for (int k = 0; k < MAXV; k++) x.m2g[k] = m2g[k];
+                        if (dn.n_new == 2) {
+                            lane::m2g_set<MAXV>(x.m2g, dn.nv - 2u, e1);
+                            lane::m2g_set<MAXV>(x.m2g, dn.nv - 1u, e2);
+                        } else if (dn.n_new == 1) {
+                            lane::m2g_set<MAXV>(x.m2g, dn.nv - 1u, e1);
+                        }
+                        x.node = hit;
+                        x.nv = dn.nv;
+                        x.tr_prev = etr;
+                        x.h = h;
+                        x.root = stk[5 * cap + pi];
+                        x.P = P;
+                    }
+                }
+            }
+            __syncwarp();
+            // ---- pop the pieces taken whole; advance the split one
+            if (lane_id == kf && kf < top && excl < T) {
+                stk[1 * cap + top - 1 - kf] += T - excl;
+                stk[2 * cap + top - 1 - kf] -= T - excl;
+            }
+            ps = top - kf;
+            __syncwarp();
+        }
+        // ---- the new partial matches' windows go on top of the stack (depth first)
+        if (__any_sync(kFull, has)) open_push<MAXV, GEN>(w, s_nodes, s_groups, stk, ps, has, x, c);
+    }
+
+    // ---- counters: lanes -> block -> global, once per block
+    __syncthreads();
+    if (s_cnt) {
+        for (uint32_t sl = tid >> 5; sl < p.n_slots; sl += kWarps) {
+            unsigned long long v = 0;
+            for (uint32_t i = lane_id; i < kWB; i += 32) v += s_cnt[sl * kWB + i];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+            if (lane_id == 0) s_tot[sl] += v;
+        }
+        __syncthreads();
+    }
+    for (uint32_t i = tid; i < p.n_motifs; i += kWB) {
+        const unsigned long long v = s_tot[s_nodes[p.motif_node[i]].slot];
+        if (v) atomicAdd(p.counts + i, v);
+    }
+}
+
+}  // namespace wdfs

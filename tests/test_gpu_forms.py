@@ -1,7 +1,8 @@
 """GPU parity of each kernel form vs the oracle, forced with MAYURA_KERNEL: "flat" (level-
 synchronous, entry-parallel; csrc/flat.cuh; the default for graphs that fit in L2),
-"hybrid" (one breadth-first level + the depth-first lane kernel; the default for larger
-graphs) and "lane" (pure depth-first).  Random groups, hub lists, the C1 workload, the
+"hybrid" (one breadth-first level + the warp-synchronous depth-first kernel, wdfs.cuh; the
+default for larger graphs), "warp" (the warp kernel straight from the roots), "lane" (the
+per-lane depth-first kernel) and "mixed".  Random groups, hub lists, the C1 workload, the
 87-motif 3-edge family (every anchor kind incl. GLOBAL), and forced overflow of the
 window-piece and frontier buffers (the depth-first fallback must keep counts exact)."""
 import numpy as np
@@ -12,7 +13,7 @@ import synth
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["flat", "hybrid", "lane", "mixed"])
+@pytest.fixture(params=["flat", "hybrid", "lane", "mixed", "warp"])
 def M(monkeypatch, request):
     import torch
     if not torch.cuda.is_available():
@@ -122,3 +123,14 @@ def test_form_family_m4(M, oracle_mod):
     got = run(M, src, dst, t, V, fam, 30)
     assert got == oracle_mod.backtrack(src, dst, t, V, fam, 30)
     assert sum(got) == _pins.family_total(src, dst, t, 4, 30)
+
+
+@pytest.mark.parametrize("cap", ["1", "6", "40"])
+def test_form_small_warp_stacks(M, oracle_mod, monkeypatch, cap):
+    """The warp kernel's piece stack at 1, 6 and 40 entries: rounds are throttled to the room
+    left and pushes past the capacity are mined depth-first by the lane (bfs::dfs) -- exact."""
+    monkeypatch.setenv("MAYURA_WDFS_CAP", cap)
+    for seed in range(2):
+        src, dst, t, V = synth.random_graph(90 + seed, 6, 6000, 3000, 0.01)
+        motifs = synth.group(synth.GROUP_C4)
+        assert run(M, src, dst, t, V, motifs, 40) == oracle_mod.backtrack(src, dst, t, V, motifs, 40)

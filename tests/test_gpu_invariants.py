@@ -17,7 +17,7 @@ import synth
 
 pytestmark = pytest.mark.gpu
 
-FORMS = ["flat", "hybrid", "lane", "mixed", "bfs"]
+FORMS = ["flat", "hybrid", "lane", "mixed", "bfs", "warp"]
 I64 = np.iinfo(np.int64)
 
 

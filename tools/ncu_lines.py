@@ -21,8 +21,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def ncu_sass(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True, check=True).stdout
+    if rep.endswith(".csv"):  # a `--page source --csv` export made on the GPU box
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                             capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     kernels = []
     i = 0

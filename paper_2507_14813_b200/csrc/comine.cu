@@ -287,17 +287,22 @@ cudaError_t launch_enum(const lane::LParams &p, uint32_t max_vertices, bool gene
 }
 
 // ---- warp-synchronous depth-first kernel (wdfs.cuh)
-// pieces per warp stack: MAYURA_WDFS_CAP overrides (test hook / tuning), else 128; at least one
-// item's worth of pieces (max_groups)
-uint32_t wdfs_cap(uint32_t max_groups) {  // read per call: tests switch it within one process
-    const char *e = getenv("MAYURA_WDFS_CAP");
-    const int v = e ? std::max(1, atoi(e)) : 128;
-    return std::max<uint32_t>((uint32_t)v, max_groups);
+// MAYURA_WDFS_SMALL=1 (test hook, read per call): the 64-piece stack instance, which spills to
+// global memory early and often
+bool wdfs_small() {
+    const char *e = getenv("MAYURA_WDFS_SMALL");
+    return e && atoi(e) != 0;
+}
+// MAYURA_WDFS_STATS=1: mayura_comine_stats runs the instrumented warp kernel (round / spill
+// counters in the stats fields, see mayura.py) instead of the instrumented lane kernel
+bool wdfs_stats() {
+    const char *e = getenv("MAYURA_WDFS_STATS");
+    return e && atoi(e) != 0;
 }
 
-template <int MAXV, bool GEN>
+template <int MAXV, bool GEN, int CAP, bool STATS>
 cudaError_t launch_wdfs_t(const wdfs::WParams &w, size_t smem, cudaStream_t s, int sms) {
-    auto kern = wdfs::wdfs_kernel<MAXV, GEN>;
+    auto kern = wdfs::wdfs_kernel<MAXV, GEN, CAP, STATS>;
     int per_sm = 0;
     cudaError_t e = blocks_per_sm((const void *)kern, wdfs::kWB, smem, &per_sm);
     if (e != cudaSuccess) return e;
@@ -306,30 +311,72 @@ cudaError_t launch_wdfs_t(const wdfs::WParams &w, size_t smem, cudaStream_t s, i
     return le != cudaSuccess ? le : cudaGetLastError();
 }
 
-template <int MAXV>
-cudaError_t launch_wdfs_v(wdfs::WParams w, bool generic, cudaStream_t s, int sms) {
+template <int MAXV, int CAP>
+cudaError_t launch_wdfs_c(wdfs::WParams w, bool generic, bool stats, cudaStream_t s, int sms) {
     const bfs::BParams &b = w.b;
     w.lanecnt = (size_t)b.n_slots * wdfs::kWB * 4 <= kLaneCntSmem ? 1u : 0u;
     w.o_cnt = (uint32_t)wdfs::off_cnt(b.n_nodes, b.n_groups, b.n_slots);
     w.o_stk = (uint32_t)wdfs::off_stk(b.n_nodes, b.n_groups, b.n_slots, w.lanecnt != 0);
-    const size_t smem = wdfs::smem_bytes<MAXV>(b.n_nodes, b.n_groups, b.n_slots, w.lanecnt != 0, w.cap);
-    return generic ? launch_wdfs_t<MAXV, true>(w, smem, s, sms) : launch_wdfs_t<MAXV, false>(w, smem, s, sms);
+    const size_t smem = wdfs::smem_bytes(b.n_nodes, b.n_groups, b.n_slots, w.lanecnt != 0, MAXV, CAP);
+    if (stats) return launch_wdfs_t<MAXV, true, CAP, true>(w, smem, s, sms);
+    return generic ? launch_wdfs_t<MAXV, true, CAP, false>(w, smem, s, sms)
+                   : launch_wdfs_t<MAXV, false, CAP, false>(w, smem, s, sms);
 }
 
-cudaError_t launch_wdfs(const wdfs::WParams &w, uint32_t max_vertices, bool generic, cudaStream_t s, int sms) {
-    if (max_vertices <= 4) return launch_wdfs_v<4>(w, generic, s, sms);
-    if (max_vertices <= 6) return launch_wdfs_v<6>(w, generic, s, sms);
-    if (max_vertices <= 8) return launch_wdfs_v<8>(w, generic, s, sms);
-    return launch_wdfs_v<16>(w, generic, s, sms);
+template <int MAXV>
+cudaError_t launch_wdfs_v(wdfs::WParams w, bool generic, bool stats, cudaStream_t s, int sms) {
+    return wdfs_small() ? launch_wdfs_c<MAXV, wdfs::kCapSmall>(w, generic, stats, s, sms)
+                        : launch_wdfs_c<MAXV, wdfs::kCap>(w, generic, stats, s, sms);
+}
+
+uint32_t mv_class(uint32_t max_vertices) {
+    return max_vertices <= 4 ? 4 : max_vertices <= 6 ? 6 : max_vertices <= 8 ? 8 : 16;
+}
+
+// Spill area of the warp kernel: per resident warp, room for the bottom halves of its stack
+// (1,024 pieces; 64 MiB - 1 GiB in total, at most 5 % of the free memory), allocated per graph.
+mayura_status ensure_wspill(mayura_graph_s *g, uint32_t mv, int sms, uint32_t *spill_cap) {
+    const size_t piece = 4 * (6 + (size_t)mv_class(mv));
+    const size_t warps = (size_t)sms * 16 * wdfs::kWarps;  // >= resident warps of any instance
+    if (!g->d_wspill) {
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        const size_t want = std::max<size_t>(64ull << 20, std::min<size_t>({1ull << 30, (size_t)(free_b * 0.05),
+                                                                          warps * 1024 * 4 * 22}));
+        CK((cudaError_t)dmalloc((void **)&g->d_wspill, want), "cudaMalloc(warp stack spill)");
+        g->wspill_bytes = want;
+        g->device_bytes += want;
+        g->fresh_alloc = true;
+    }
+    *spill_cap = (uint32_t)std::min<size_t>(g->wspill_bytes / (warps * piece), 0xFFFFFFFFu);
+    // test hook: a tiny spill area forces the depth-first fallback of full stacks
+    if (const char *e = getenv("MAYURA_WDFS_SPILL_CAP")) *spill_cap = std::min<uint32_t>(*spill_cap, (uint32_t)atoi(e));
+    return MAYURA_OK;
+}
+
+mayura_status launch_wdfs(mayura_graph_s *g, wdfs::WParams w, uint32_t max_vertices, bool generic, bool stats,
+                          cudaStream_t s, int sms) {
+    mayura_status ms = ensure_wspill(g, max_vertices, sms, &w.spill_cap);
+    if (ms != MAYURA_OK) return ms;
+    if (g->fresh_alloc) {
+        CK(cudaStreamSynchronize(0), "cudaStreamSynchronize");
+        g->fresh_alloc = false;
+    }
+    w.spill = g->d_wspill;
+    cudaError_t e;
+    if (max_vertices <= 4) e = launch_wdfs_v<4>(w, generic, stats, s, sms);
+    else if (max_vertices <= 6) e = launch_wdfs_v<6>(w, generic, stats, s, sms);
+    else if (max_vertices <= 8) e = launch_wdfs_v<8>(w, generic, stats, s, sms);
+    else e = launch_wdfs_v<16>(w, generic, stats, s, sms);
+    CK(e, "wdfs_kernel launch");
+    return MAYURA_OK;
 }
 
 // the warp kernel's stacks fit the block's shared memory (else the lane kernel is used)
 bool wdfs_fits(const DeviceTable &dt) {
-    const uint32_t mv = dt.max_vertices <= 4 ? 4 : dt.max_vertices <= 6 ? 6 : dt.max_vertices <= 8 ? 8 : 16;
     const bool lc = (size_t)dt.n_slots * wdfs::kWB * 4 <= kLaneCntSmem;
-    const size_t bytes = wdfs::off_stk(dt.n_nodes, dt.n_groups, dt.n_slots, lc) +
-                         (size_t)wdfs::kWarps * (6 + mv) * wdfs_cap(dt.max_groups) * 4;
-    return bytes <= 160 * 1024;
+    return wdfs::smem_bytes(dt.n_nodes, dt.n_groups, dt.n_slots, lc, (int)mv_class(dt.max_vertices), wdfs::kCap) <=
+           200 * 1024;
 }
 
 // depth-first phase: MAYURA_DFS=lane selects the lane kernel (A/B), default the warp kernel
@@ -786,17 +833,14 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         CK(launch_lane(q, dt.max_vertices, false, dt.generic, s, sms), "comine_lane_kernel launch");
         return MAYURA_OK;
     }
-    if (kind == K_WARP && !st && wdfs_fits(dt)) {  // the warp kernel straight from the root edges
+    if (kind == K_WARP && (!st || wdfs_stats()) && wdfs_fits(dt)) {  // the warp kernel straight from the roots
         wdfs::WParams w;
-        w.b = bfs_params(g, dt, r0, n_roots, counts, nullptr, 0u);
+        w.b = bfs_params(g, dt, r0, n_roots, counts, stats, 0u);
         w.b.in.data = nullptr;
         w.gwant = dt.gwant;
         w.lb = lb;
         w.direct = 1;
-        w.cap = wdfs_cap(dt.max_groups);
-        w.max_groups = dt.max_groups;
-        CK(launch_wdfs(w, dt.max_vertices, dt.generic, s, sms), "wdfs_kernel launch");
-        return MAYURA_OK;
+        return launch_wdfs(g, w, dt.max_vertices, dt.generic, st, s, sms);
     }
     if (kind == K_FLAT || kind == K_MIXED) levels = std::min(hybrid_levels(), dt.max_edges > 2 ? dt.max_edges - 2 : 0u);
     lane::LParams q = lane_params(g, dt, r0, n_roots, lb, counts, stats, st);
@@ -811,7 +855,7 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         uint32_t *bufs[2] = {g->d_bfs[0], g->d_bfs[1]};
         CK(launch_bfs(b, dt.max_vertices, levels, bufs, ctl, g->bfs_seg_cap, st, s, sms), "bfs pass launch");
         if (kind == K_BFS) return MAYURA_OK;
-        if (kind == K_HYBRID && levels == 1 && !st && use_wdfs() && wdfs_fits(dt)) {
+        if (kind == K_HYBRID && levels == 1 && (!st || wdfs_stats()) && use_wdfs() && wdfs_fits(dt)) {
             // depth-first phase in the warp kernel: items = the level's partial matches + light roots
             wdfs::WParams w;
             w.b = b;
@@ -821,10 +865,7 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
             w.gwant = dt.gwant;
             w.lb = lb;
             w.direct = 0;
-            w.cap = wdfs_cap(dt.max_groups);
-            w.max_groups = dt.max_groups;
-            CK(launch_wdfs(w, dt.max_vertices, dt.generic, s, sms), "wdfs_kernel launch");
-            return MAYURA_OK;
+            return launch_wdfs(g, w, dt.max_vertices, dt.generic, st, s, sms);
         }
         q.pm = bufs[(levels - 1) & 1];
         q.pm_cnt = ctl + (levels - 1) * kCtlWords;
@@ -1248,14 +1289,14 @@ struct ScratchSet {
     size_t bfs_bytes = 0;
     int bfs_nbufs = 0;
     uint32_t bfs_words = 0, bfs_seg_cap = 0, bfs_long_cap = 0;
-    uint32_t *ctl = nullptr, *lng = nullptr, *light = nullptr, *flat_win = nullptr, *queue = nullptr;
-    uint64_t flat_win_bytes = 0, bytes = 0;
+    uint32_t *ctl = nullptr, *lng = nullptr, *light = nullptr, *flat_win = nullptr, *queue = nullptr, *wspill = nullptr;
+    uint64_t flat_win_bytes = 0, bytes = 0, wspill_bytes = 0;
 };
 std::mutex g_scratch_mu;
 ScratchSet g_scratch[64];
 
 void free_scratch_set(ScratchSet &c) {
-    void *ptrs[] = {c.bfs[0], c.bfs[1], c.ctl, c.lng, c.light, c.flat_win, c.queue};
+    void *ptrs[] = {c.bfs[0], c.bfs[1], c.ctl, c.lng, c.light, c.flat_win, c.queue, c.wspill};
     for (void *p : ptrs) dfree(p);
     c = ScratchSet();
 }
@@ -1275,8 +1316,9 @@ void stash_scratch(mayura_graph_s *g) {
     c.ctl = g->d_bfs_ctl; c.lng = g->d_bfs_long; c.light = g->d_light;
     c.flat_win = g->d_flat_win; c.flat_win_bytes = g->flat_win_bytes;
     c.queue = g->d_queue;
+    c.wspill = g->d_wspill; c.wspill_bytes = g->wspill_bytes;
     g->d_bfs[0] = g->d_bfs[1] = nullptr;
-    g->d_bfs_ctl = g->d_bfs_long = g->d_light = g->d_flat_win = g->d_queue = nullptr;
+    g->d_bfs_ctl = g->d_bfs_long = g->d_light = g->d_flat_win = g->d_queue = g->d_wspill = nullptr;
 }
 
 // before building a graph of E edges on `device`: drop a cached set too small for it (so its
@@ -1304,8 +1346,9 @@ void adopt_scratch(mayura_graph_s *g) {
     g->d_bfs_ctl = c.ctl; g->d_bfs_long = c.lng; g->d_light = c.light;
     g->d_flat_win = c.flat_win; g->flat_win_bytes = c.flat_win_bytes;
     g->d_queue = c.queue;
+    g->d_wspill = c.wspill; g->wspill_bytes = c.wspill_bytes;
     g->device_bytes += (uint64_t)c.bfs_nbufs * c.bfs_bytes + c.flat_win_bytes + 4ull * 3 * c.bfs_long_cap +
-                       4ull * (c.e_cap + 32);
+                       4ull * (c.e_cap + 32) + c.wspill_bytes;
     c = ScratchSet();
 }
 
@@ -1315,7 +1358,7 @@ void free_device(mayura_graph_s *g) {
     cudaDeviceSynchronize();  // no queued work may still use the memory returned to the pool
     stash_scratch(g);
     void *ptrs[] = {g->d_arena, g->d_queue, g->d_counts, g->d_stats, g->d_dbg, g->d_bfs[0], g->d_bfs[1],
-                    g->d_bfs_ctl, g->d_bfs_long, g->d_light, g->d_enum, g->d_flat_win};  // arena: graph arrays
+                    g->d_bfs_ctl, g->d_bfs_long, g->d_light, g->d_enum, g->d_flat_win, g->d_wspill};  // arena: graph arrays
     for (void *p : ptrs) dfree(p);
     cudaStreamSynchronize(0);
 }

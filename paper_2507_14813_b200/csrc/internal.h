@@ -100,6 +100,8 @@ struct mayura_graph_s {
     uint32_t *d_flat_win = nullptr;                      // flat form: window pieces (uint4)
     uint64_t flat_win_bytes = 0;
     uint32_t *d_light = nullptr;                         // hybrid: light roots listed by the BFS level (E + 32)
+    uint32_t *d_wspill = nullptr;                        // warp kernel: per-warp stack spill area
+    uint64_t wspill_bytes = 0;
     size_t bfs_bytes = 0;
     int bfs_nbufs = 0;
     uint32_t bfs_words = 0;

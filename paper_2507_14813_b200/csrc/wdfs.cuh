@@ -33,10 +33,13 @@ namespace wdfs {
 
 constexpr int kWB = 128;                 // threads per block
 constexpr int kWarps = kWB / 32;
+constexpr int kCap = 128;                // pieces per warp stack in shared memory
+constexpr int kCapSmall = 64;            // test instance (MAYURA_WDFS_SMALL=1): spills early and often
 
 template <int MAXV>
 struct Piece {
-    // SoA words per piece: 0 group, 1 pos, 2 n, 3 tr_prev, 4 h, 5 root, 6.. m2g[MAXV]
+    // words per piece: 0 group, 1 pos, 2 n, 3 tr_prev, 4 h, 5 root, 6.. m2g[MAXV]
+    // (shared memory: SoA, field f of piece i at f * CAP + i; spill area: AoS, F words per piece)
     static constexpr int F = 6 + MAXV;
 };
 
@@ -45,9 +48,9 @@ struct WParams {
                              // level's partial-match records (hybrid), b.light = its light roots
     const uint32_t *gwant;   // per group: wants of its first 4 children (bytes, 0xFD pad)
     uint32_t *lb;            // [0]: item cursor (zeroed per query by the launcher)
+    uint32_t *spill;         // per warp spill_cap pieces (AoS): the bottom of a full stack
+    uint32_t spill_cap;
     uint32_t direct;         // 1: the items are the root edges [r0, r0 + n_roots) themselves
-    uint32_t cap;            // pieces per warp stack
-    uint32_t max_groups;     // anchor groups of the widest node
     uint32_t o_cnt, o_stk;   // dynamic shared memory offsets: lane counters, stacks
     uint32_t lanecnt;        // 1: per-lane u32 counters; 0: block u64 atomics (many slots)
 };
@@ -59,9 +62,8 @@ __host__ __device__ inline size_t off_cnt(uint32_t nn, uint32_t ng, uint32_t ns)
 __host__ __device__ inline size_t off_stk(uint32_t nn, uint32_t ng, uint32_t ns, bool lanecnt) {
     return lane::align16(off_cnt(nn, ng, ns) + (lanecnt ? (size_t)ns * kWB * 4 : 0));
 }
-template <int MAXV>
-__host__ __device__ inline size_t smem_bytes(uint32_t nn, uint32_t ng, uint32_t ns, bool lanecnt, uint32_t cap) {
-    return off_stk(nn, ng, ns, lanecnt) + (size_t)kWarps * Piece<MAXV>::F * cap * 4;
+__host__ __device__ inline size_t smem_bytes(uint32_t nn, uint32_t ng, uint32_t ns, bool lanecnt, int maxv, int cap) {
+    return off_stk(nn, ng, ns, lanecnt) + (size_t)kWarps * (6 + maxv) * cap * 4;
 }
 
 // Upper bound of a window's length: entries [lo, lo + n) contain every entry of the window
@@ -77,7 +79,7 @@ __device__ __forceinline__ uint32_t window_len_ub(const uint2 *ent, uint32_t lo,
 #pragma unroll
     for (int k = 5; k >= 0; k--)
         if (lo + o[k] >= sent || v[k] > h) n = o[k];
-    if (n != kNone) return n;
+    if (n != kNone) return min(n, sent - lo);  // never past the sentinel: the next list follows it
     // >= 32 entries: gallop (dependent loads, rare), then bisect to a bracket of <= 32
     uint32_t a = 31, b = 63;
     for (;;) {
@@ -136,15 +138,53 @@ __device__ __forceinline__ uint32_t window(const bfs::BParams &p, const DGroup &
     return lo;
 }
 
+// Warp-collective: move the bottom m pieces of the shared-memory stack to the warp's spill area
+// (coalesced AoS writes) and shift the rest down, 32 pieces at a time in ascending order, each
+// chunk read before it is written (no chunk's destination overlaps a later chunk's source).
+template <int MAXV, int CAP>
+__device__ __noinline__ void spill_bottom(uint32_t *stk, uint32_t ps, uint32_t m, uint32_t *sp, uint32_t sp_top) {
+    constexpr int F = Piece<MAXV>::F;
+    const uint32_t lane_id = threadIdx.x & 31;
+    for (uint32_t wi = lane_id; wi < m * F; wi += 32) {
+        const uint32_t i = wi / F, f = wi - i * F;
+        sp[(size_t)(sp_top + i) * F + f] = stk[f * CAP + i];
+    }
+    __syncwarp();
+    for (uint32_t c = 0; c < ps - m; c += 32) {
+        const uint32_t i = c + lane_id;
+        uint32_t t[F];
+#pragma unroll
+        for (int f = 0; f < F; f++) t[f] = i < ps - m ? stk[f * CAP + m + i] : 0u;
+        __syncwarp();
+        if (i < ps - m)
+#pragma unroll
+            for (int f = 0; f < F; f++) stk[f * CAP + i] = t[f];
+        __syncwarp();
+    }
+}
+
+// Warp-collective: move the top m pieces of the spill area onto the (empty) stack.
+template <int MAXV, int CAP>
+__device__ __noinline__ void reload(uint32_t *stk, uint32_t m, const uint32_t *sp, uint32_t sp_top) {
+    constexpr int F = Piece<MAXV>::F;
+    const uint32_t lane_id = threadIdx.x & 31;
+    for (uint32_t wi = lane_id; wi < m * F; wi += 32) {
+        const uint32_t i = wi / F, f = wi - i * F;
+        stk[f * CAP + i] = sp[(size_t)(sp_top - m + i) * F + f];
+    }
+    __syncwarp();
+}
+
 // Warp-collective: every lane with `has` locates the windows of x's anchor groups and pushes the
-// non-empty ones on the warp's stack (warp-aggregated).  A push past the capacity makes the lane
-// mine x from that group on depth-first itself (exact; counted in p.fallback).
-template <int MAXV, bool GEN>
+// non-empty ones on the warp's stack (warp-aggregated).  A full stack spills its bottom half to
+// global memory; a full spill area makes the lane mine x from that group on depth-first itself
+// (exact; counted in p.fallback).
+template <int MAXV, bool GEN, int CAP, bool STATS>
 __device__ __forceinline__ void open_push(const WParams &w, const lane::LNode *s_nodes, const DGroup *s_groups,
-                                          uint32_t *stk, uint32_t &ps, bool has, const bfs::PM<MAXV> &x,
-                                          bfs::Ctx &c) {
+                                          uint32_t *stk, uint32_t &ps, uint32_t *sp, uint32_t &sp_top, bool has,
+                                          const bfs::PM<MAXV> &x, bfs::Ctx &c) {
     const bfs::BParams &p = w.b;
-    const uint32_t lane_id = threadIdx.x & 31, cap = w.cap;
+    const uint32_t lane_id = threadIdx.x & 31;
     uint32_t gb = 0, ng = 0;
     if (has) {
         const lane::LNode xn = s_nodes[x.node];
@@ -159,32 +199,39 @@ __device__ __forceinline__ void open_push(const WParams &w, const lane::LNode *s
         if (mine) lo = window<MAXV, GEN>(p, s_groups[gb + q], x, n);
         const bool v = mine && n > 0;
         const unsigned bm = __ballot_sync(kFull, v);
+        const uint32_t cnt = __popc(bm);
+        if (ps + cnt > CAP && ps >= 2 && sp_top + ps / 2 <= w.spill_cap) {
+            spill_bottom<MAXV, CAP>(stk, ps, ps / 2, sp, sp_top);
+            sp_top += ps / 2;
+            ps -= ps / 2;
+            if (STATS && lane_id == 0) c.st[ST_OFFLOADS]++;
+        }
         const uint32_t slot = ps + __popc(bm & ((1u << lane_id) - 1u));
         if (v) {
-            if (slot < cap) {
-                stk[0 * cap + slot] = gb + q;
-                stk[1 * cap + slot] = lo;
-                stk[2 * cap + slot] = n;
-                stk[3 * cap + slot] = x.tr_prev;
-                stk[4 * cap + slot] = x.h;
-                stk[5 * cap + slot] = x.root;
+            if (slot < CAP) {
+                stk[0 * CAP + slot] = gb + q;
+                stk[1 * CAP + slot] = lo;
+                stk[2 * CAP + slot] = n;
+                stk[3 * CAP + slot] = x.tr_prev;
+                stk[4 * CAP + slot] = x.h;
+                stk[5 * CAP + slot] = x.root;
 #pragma unroll
-                for (int k = 0; k < MAXV; k++) stk[(6 + k) * cap + slot] = x.m2g[k];
+                for (int k = 0; k < MAXV; k++) stk[(6 + k) * CAP + slot] = x.m2g[k];
             } else {
                 atomicAdd(p.fallback, 1u);
                 bfs::dfs<MAXV, false>(p, s_nodes, s_groups, x, c, gb + q);
                 fell = true;
             }
         }
-        ps = min(ps + (uint32_t)__popc(bm), cap);
+        ps = min(ps + cnt, (uint32_t)CAP);
+        if (STATS && lane_id == 0) c.st[ST_WINDOWS] += cnt;
     }
     __syncwarp();
 }
 
-template <int MAXV, bool GEN>
+template <int MAXV, bool GEN, int CAP, bool STATS>
 __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WParams w) {
     pdl_begin();
-    constexpr int F = Piece<MAXV>::F;
     const bfs::BParams &p = w.b;
     extern __shared__ __align__(16) unsigned char smem[];
     lane::LNode *s_nodes = reinterpret_cast<lane::LNode *>(smem);
@@ -192,8 +239,10 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
     unsigned long long *s_tot = reinterpret_cast<unsigned long long *>(
         smem + lane::align16((size_t)p.n_nodes * sizeof(lane::LNode)) + lane::align16((size_t)p.n_groups * sizeof(DGroup)));
     uint32_t *s_cnt = w.lanecnt ? reinterpret_cast<uint32_t *>(smem + w.o_cnt) : nullptr;
-    const uint32_t tid = threadIdx.x, lane_id = tid & 31, cap = w.cap;
-    uint32_t *stk = reinterpret_cast<uint32_t *>(smem + w.o_stk) + (size_t)(tid >> 5) * F * cap;
+    const uint32_t tid = threadIdx.x, lane_id = tid & 31;
+    constexpr int F = Piece<MAXV>::F;
+    uint32_t *stk = reinterpret_cast<uint32_t *>(smem + w.o_stk) + (size_t)(tid >> 5) * F * CAP;
+    uint32_t *sp = w.spill + (size_t)(blockIdx.x * kWarps + (tid >> 5)) * w.spill_cap * F;
     __shared__ uint32_t s_gw[lane::kGwMax];
     __shared__ uint32_t s_pref[bfs::kStripes + 1];
     for (uint32_t i = tid; i < p.n_nodes; i += kWB) s_nodes[i] = p.nodes[i];
@@ -224,13 +273,14 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
     const uint32_t n_pm = s_pref[bfs::kStripes];
     const uint32_t n_items = w.direct ? p.n_roots : n_pm + (p.light ? *(volatile const uint32_t *)p.light_cnt : 0u);
 
-    uint32_t ps = 0;           // warp-uniform stack height
+    uint32_t ps = 0;           // warp-uniform stack height (shared memory)
+    uint32_t sp_top = 0;       // warp-uniform spilled pieces (global memory)
     uint32_t cb = 0, cl = 0;   // warp-uniform item chunk
     bool items_left = true;
     for (;;) {
         // ---- the top pieces: candidate counts and their running sum (top first)
         const uint32_t top = ps;
-        const uint32_t pn = lane_id < top ? stk[2 * cap + top - 1 - lane_id] : 0u;
+        const uint32_t pn = lane_id < top ? stk[2 * CAP + top - 1 - lane_id] : 0u;
         uint32_t incl = pn;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -241,9 +291,17 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
 
         bfs::PM<MAXV> x;   // this lane's new partial match: an item, or a child found this round
         bool has = false;
-        if (tot < 32 && items_left && top + w.max_groups <= cap) {
-            // ---- fewer than 32 candidates stacked: take the next items (one per lane, up to 32, as
-            // many as the stack has room for if each pushes max_groups pieces)
+        if (top == 0 && sp_top > 0) {
+            // ---- the stack ran empty: bring back the most recently spilled pieces (depth first)
+            const uint32_t m = min(sp_top, (uint32_t)CAP / 2);
+            reload<MAXV, CAP>(stk, m, sp, sp_top);
+            sp_top -= m;
+            ps = m;
+            if (STATS && lane_id == 0) c.st[ST_CONTEXTS]++;
+            continue;
+        }
+        if (tot < 32 && items_left && sp_top == 0) {
+            // ---- fewer than 32 candidates stacked: take the next items (one per lane)
             if (cl == 0) {
                 uint32_t b = 0, sz = 0;
                 if (lane_id == 0) {
@@ -261,7 +319,7 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
                 cb = b;
                 cl = min(sz, n_items - b);
             }
-            const uint32_t take = min(min(32u, cl), (cap - top) / w.max_groups);
+            const uint32_t take = min(32u, cl);
             const uint32_t item = cb + lane_id;
             cb += take;
             cl -= take;
@@ -279,12 +337,11 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
                     has = bfs::load_root<MAXV>(p, __ldg(p.light + (item - n_pm)), x);
                 }
             }
+            if (STATS && lane_id == 0) c.st[ST_ROOTS] += take;
         } else {
-            if (top == 0) break;  // no items left and nothing stacked
-            // ---- this round: T entries, one per lane, from the top pieces (the last one possibly
-            // split).  Throttle: every entry may push up to max_groups pieces; keep them in the stack.
-            const uint32_t room = cap - top;
-            const uint32_t T = min(min(tot, 32u), max(1u, room / max(1u, w.max_groups)));
+            if (top == 0) break;  // no items left, nothing stacked or spilled
+            // ---- this round: T entries, one per lane, from the top pieces (the last one possibly split)
+            const uint32_t T = min(tot, 32u);
             const uint32_t excl = incl - pn;
             const bool pc = lane_id < top && excl < T;  // this piece contributes entries
             const uint32_t smask = __reduce_or_sync(kFull, pc ? (1u << excl) : 0u);
@@ -293,14 +350,15 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
             const uint32_t upto = smask & ((2u << lane_id) - 1u);
             const uint32_t pi = top - 1 - (act ? (uint32_t)__popc(upto) - 1u : 0u);  // this lane's piece
             const uint32_t at = lane_id - (31 - __clz(upto | 1u));                    // offset in the piece
+            bool valid = false;
             if (act) {
-                const uint32_t g = stk[0 * cap + pi];
-                const uint32_t pos = stk[1 * cap + pi] + at;
-                const uint32_t tp = stk[3 * cap + pi];
-                const uint32_t h = stk[4 * cap + pi];
+                const uint32_t g = stk[0 * CAP + pi];
+                const uint32_t pos = stk[1 * CAP + pi] + at;
+                const uint32_t tp = stk[3 * CAP + pi];
+                const uint32_t h = stk[4 * CAP + pi];
                 uint32_t m2g[MAXV];
 #pragma unroll
-                for (int k = 0; k < MAXV; k++) m2g[k] = stk[(6 + k) * cap + pi];
+                for (int k = 0; k < MAXV; k++) m2g[k] = stk[(6 + k) * CAP + pi];
                 const DGroup G = s_groups[g];
                 const bool glob = GEN && G.kind == ANCHOR_GLOBAL;
                 uint32_t etr, e1, e2 = 0;
@@ -317,7 +375,7 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
                     e1 = e.y;
                     if (G.n_inner) P = __ldg((out ? p.out_ptr : p.in_ptr) + pos);  // with the entry
                 }
-                const bool valid = etr > tp && etr <= h;
+                valid = etr > tp && etr <= h;
                 uint32_t cls;
                 if (glob)
                     cls = (e1 != e2 && lane::classify<MAXV>(m2g, e1) == CLS_NEW &&
@@ -334,6 +392,7 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
                 if (valid && hit != kNone) {
                     const lane::LNode dn = s_nodes[hit];
                     if (dn.flags & NODE_COMPLETION) bfs::count_add(c, dn.slot, 1);
+                    if (STATS) c.st[ST_MATCHES] += (dn.flags & NODE_COMPLETION) ? 1 : 0;
                     if (dn.flags & NODE_INNER) {  // the child partial match (Algo 3 l.665-669)
                         has = true;
 #pragma unroll
@@ -348,22 +407,31 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
                         x.nv = dn.nv;
                         x.tr_prev = etr;
                         x.h = h;
-                        x.root = stk[5 * cap + pi];
+                        x.root = stk[5 * CAP + pi];
                         x.P = P;
+                        if (STATS) c.st[ST_NODES]++;
                     }
+                }
+            }
+            if (STATS) {
+                const uint32_t nv = __popc(__ballot_sync(kFull, valid));
+                if (lane_id == 0) {
+                    c.st[ST_BATCHES]++;
+                    c.st[ST_PROBES] += T;
+                    c.st[ST_ENTRIES] += nv;
                 }
             }
             __syncwarp();
             // ---- pop the pieces taken whole; advance the split one
             if (lane_id == kf && kf < top && excl < T) {
-                stk[1 * cap + top - 1 - kf] += T - excl;
-                stk[2 * cap + top - 1 - kf] -= T - excl;
+                stk[1 * CAP + top - 1 - kf] += T - excl;
+                stk[2 * CAP + top - 1 - kf] -= T - excl;
             }
             ps = top - kf;
             __syncwarp();
         }
         // ---- the new partial matches' windows go on top of the stack (depth first)
-        if (__any_sync(kFull, has)) open_push<MAXV, GEN>(w, s_nodes, s_groups, stk, ps, has, x, c);
+        if (__any_sync(kFull, has)) open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, has, x, c);
     }
 
     // ---- counters: lanes -> block -> global, once per block
@@ -381,6 +449,15 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
     for (uint32_t i = tid; i < p.n_motifs; i += kWB) {
         const unsigned long long v = s_tot[s_nodes[p.motif_node[i]].slot];
         if (v) atomicAdd(p.counts + i, v);
+    }
+    if (STATS) {
+#pragma unroll
+        for (int i = 0; i < ST_N; i++) {
+            unsigned long long v = c.st[i];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+            if (lane_id == 0 && v) atomicAdd(p.stats + i, v);
+        }
     }
 }
 

@@ -125,11 +125,15 @@ def test_form_family_m4(M, oracle_mod):
     assert sum(got) == _pins.family_total(src, dst, t, 4, 30)
 
 
-@pytest.mark.parametrize("cap", ["1", "6", "40"])
-def test_form_small_warp_stacks(M, oracle_mod, monkeypatch, cap):
-    """The warp kernel's piece stack at 1, 6 and 40 entries: rounds are throttled to the room
-    left and pushes past the capacity are mined depth-first by the lane (bfs::dfs) -- exact."""
-    monkeypatch.setenv("MAYURA_WDFS_CAP", cap)
+@pytest.mark.parametrize("hook", ["MAYURA_WDFS_SMALL=1", "MAYURA_WDFS_SMALL=1 MAYURA_WDFS_SPILL_CAP=0",
+                                  "MAYURA_WDFS_SMALL=1 MAYURA_WDFS_SPILL_CAP=40"])
+def test_form_small_warp_stacks(M, oracle_mod, monkeypatch, hook):
+    """The warp kernel's piece stack at 64 entries: full stacks spill their bottom half to the
+    per-warp global spill area and reload it when they run empty; with no (or a 40-piece) spill
+    area the pushes past the capacity are mined depth-first by the lane (bfs::dfs) -- exact."""
+    for kv in hook.split():
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
     for seed in range(2):
         src, dst, t, V = synth.random_graph(90 + seed, 6, 6000, 3000, 0.01)
         motifs = synth.group(synth.GROUP_C4)

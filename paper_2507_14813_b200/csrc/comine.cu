@@ -152,7 +152,26 @@ std::vector<lane::LNode> lane_nodes(const Table &t, uint32_t &n_slots) {
         b.want = a.want; b.n_new = a.n_new; b.nv = a.nv; b.flags = a.flags;
         b.group_begin = a.group_begin; b.group_end = a.group_end;
         b.slot = (a.flags & NODE_COMPLETION) ? (uint16_t)n_slots++ : (uint16_t)0xFFFF;
-        b.pad = 0;
+        // Same-list groups (wdfs.cuh): node i was matched as an entry of its parent's group G; a
+        // group of i with G's kind and anchor scans the same adjacency list, and its window starts
+        // right after that entry (START_P0 = out(src), START_P1 = in(dst) of i's own edge) and ends
+        // where G's window ends (same hi(root)) -- a suffix of the parent's window.
+        b.same = 0;
+        for (uint32_t pg = 0; pg < t.groups.size(); pg++) {
+            const DGroup &G = t.groups[pg];
+            if (i < G.child_begin || i >= G.child_end || G.kind == ANCHOR_GLOBAL) continue;
+            for (uint32_t q = 0; q < (uint32_t)(a.group_end - a.group_begin) && q < 16; q++) {
+                const DGroup &G2 = t.groups[a.group_begin + q];
+                const uint8_t want_start = G.kind == ANCHOR_OUT ? START_P0 : START_P1;
+                if (G2.kind == G.kind && G2.anchor == G.anchor && G2.start == want_start) b.same |= (uint16_t)(1u << q);
+            }
+        }
+        // NODE_NEEDP: some group of this node starts from the successor pointers of its own edge
+        // and is not a same-list continuation (the warp kernel loads P with the entry only then)
+        for (uint32_t q = 0; q < (uint32_t)(a.group_end - a.group_begin); q++) {
+            const DGroup &G2 = t.groups[a.group_begin + q];
+            if (G2.start < START_R0 && !(q < 16 && ((b.same >> q) & 1u))) b.flags |= wdfs::NODE_NEEDP;
+        }
         if (a.flags & NODE_INNER) {  // pre-leaf: every child is a leaf
             bool pre = true;
             for (uint32_t gi = a.group_begin; gi < a.group_end; gi++)

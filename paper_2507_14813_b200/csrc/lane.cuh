@@ -44,7 +44,8 @@ struct __align__(4) LNode {  // 12 bytes
     uint8_t want, n_new, nv, flags;
     uint16_t group_begin, group_end;
     uint16_t slot;                      // completion counter slot (0xFFFF: none)
-    uint16_t pad;
+    uint16_t same;                      // bit q: group q of this node scans the same list as the
+                                        // group this node was matched in (wdfs.cuh continuation)
 };
 
 struct LParams {

@@ -35,6 +35,8 @@ constexpr int kWB = 128;                 // threads per block
 constexpr int kWarps = kWB / 32;
 constexpr int kCap = 128;                // pieces per warp stack in shared memory
 constexpr int kCapSmall = 64;            // test instance (MAYURA_WDFS_SMALL=1): spills early and often
+constexpr uint8_t NODE_NEEDP = 16;       // LNode flag: a group of the node needs its edge's successor
+                                         // pointers (a START_P* group that is not a same-list continuation)
 
 template <int MAXV>
 struct Piece {
@@ -66,41 +68,50 @@ __host__ __device__ inline size_t smem_bytes(uint32_t nn, uint32_t ng, uint32_t 
     return off_stk(nn, ng, ns, lanecnt) + (size_t)kWarps * (6 + maxv) * cap * 4;
 }
 
-// Upper bound of a window's length: entries [lo, lo + n) contain every entry of the window
-// (time rank <= h, before the list's sentinel at `sent`), with at most 31 entries past it.
-__device__ __forceinline__ uint32_t window_len_ub(const uint2 *ent, uint32_t lo, uint32_t sent, uint32_t h) {
-    // six independent loads (lists are padded past their last sentinel, so lo + 31 is in bounds);
-    // an index at or past the sentinel is out of the window whatever it holds
+// Length of a window: entries [lo, lo + n) are the entries of list `ent` from lo with time
+// rank <= h, stopping at the list's sentinel (index `sent`).  Six independent probes at offsets
+// 0, 1, 3, 7, 15, 31 bracket n (lists are padded past their last sentinel, so lo + 31 is in
+// bounds; an index at or past the sentinel is out whatever it holds); a bisection inside the
+// bracket makes it exact (<= 4 dependent loads on lines the probes just brought in).  Windows of
+// >= 32 entries gallop first (rare).
+__device__ __forceinline__ bool in_window(const uint2 *ent, uint32_t lo, uint32_t o, uint32_t sent, uint32_t h) {
+    return lo + o < sent && __ldg(&ent[lo + o].x) <= h;
+}
+__device__ __forceinline__ uint32_t window_len(const uint2 *ent, uint32_t lo, uint32_t sent, uint32_t h) {
     const uint32_t o[6] = {0, 1, 3, 7, 15, 31};
     uint32_t v[6];
 #pragma unroll
     for (int k = 0; k < 6; k++) v[k] = __ldg(&ent[lo + o[k]].x);
-    uint32_t n = kNone;
+    uint32_t b = kNone, a = 0;  // out at offset b; in at every probe below it
 #pragma unroll
     for (int k = 5; k >= 0; k--)
-        if (lo + o[k] >= sent || v[k] > h) n = o[k];
-    if (n != kNone) return min(n, sent - lo);  // never past the sentinel: the next list follows it
-    // >= 32 entries: gallop (dependent loads, rare), then bisect to a bracket of <= 32
-    uint32_t a = 31, b = 63;
-    for (;;) {
-        if (lo + b >= sent) {
-            b = sent - lo;
-            break;
+        if (lo + o[k] >= sent || v[k] > h) b = o[k];
+    if (b == 0) return 0;
+    if (b != kNone) {
+        a = b == 1 ? 0 : (b - 1) / 2;  // the previous probe offset (in)
+    } else {  // >= 32 entries: gallop
+        a = 31;
+        b = 63;
+        for (;;) {
+            if (lo + b >= sent) {
+                b = sent - lo;
+                break;
+            }
+            if (__ldg(&ent[lo + b].x) > h) break;
+            a = b;
+            b = 2 * b + 1;
         }
-        if (__ldg(&ent[lo + b].x) > h) break;
-        a = b;
-        b = 2 * b + 1;
     }
-    while (b - a > 32) {
+    while (b - a > 1) {  // in(a), out(b): n in (a, b]
         const uint32_t m = a + ((b - a) >> 1);
-        if (__ldg(&ent[lo + m].x) <= h) a = m;
+        if (in_window(ent, lo, m, sent, h)) a = m;
         else b = m;
     }
     return b;
 }
 
-// Window of group G for partial match x: first candidate position (exact) and a candidate count
-// covering the window (exact for the all-edges anchor).
+// Window of group G for partial match x: first position and length (exact up to entries tied
+// with tr_prev, which the time test skips).
 template <int MAXV, bool GEN>
 __device__ __forceinline__ uint32_t window(const bfs::BParams &p, const DGroup &G, const bfs::PM<MAXV> &x,
                                            uint32_t &n) {
@@ -134,7 +145,7 @@ __device__ __forceinline__ uint32_t window(const bfs::BParams &p, const DGroup &
         }
         lo = a;
     }
-    n = window_len_ub(ent, lo, sent, x.h);
+    n = window_len(ent, lo, sent, x.h);
     return lo;
 }
 
@@ -179,24 +190,35 @@ __device__ __noinline__ void reload(uint32_t *stk, uint32_t m, const uint32_t *s
 // non-empty ones on the warp's stack (warp-aggregated).  A full stack spills its bottom half to
 // global memory; a full spill area makes the lane mine x from that group on depth-first itself
 // (exact; counted in p.fallback).
+// A child matched at list position c_lo - 1 of its parent's window [.., c_end) continues on the
+// same list in every group flagged in its node's `same` mask: that window is [c_lo, c_end), no
+// memory access needed (items from a global cursor pass c_end = 0: no continuation).
 template <int MAXV, bool GEN, int CAP, bool STATS>
 __device__ __forceinline__ void open_push(const WParams &w, const lane::LNode *s_nodes, const DGroup *s_groups,
                                           uint32_t *stk, uint32_t &ps, uint32_t *sp, uint32_t &sp_top, bool has,
-                                          const bfs::PM<MAXV> &x, bfs::Ctx &c) {
+                                          const bfs::PM<MAXV> &x, uint32_t c_lo, uint32_t c_end, bfs::Ctx &c) {
     const bfs::BParams &p = w.b;
     const uint32_t lane_id = threadIdx.x & 31;
-    uint32_t gb = 0, ng = 0;
+    uint32_t gb = 0, ng = 0, same = 0;
     if (has) {
         const lane::LNode xn = s_nodes[x.node];
         gb = xn.group_begin;
         ng = xn.group_end - xn.group_begin;
+        same = c_end ? xn.same : 0u;
     }
     const uint32_t mg = __reduce_max_sync(kFull, ng);
     bool fell = false;
     for (uint32_t q = 0; q < mg; q++) {
         uint32_t lo = 0, n = 0;
         const bool mine = q < ng && !fell;
-        if (mine) lo = window<MAXV, GEN>(p, s_groups[gb + q], x, n);
+        if (mine) {
+            if ((same >> q) & 1u) {
+                lo = c_lo;
+                n = c_end > c_lo ? c_end - c_lo : 0u;
+            } else {
+                lo = window<MAXV, GEN>(p, s_groups[gb + q], x, n);
+            }
+        }
         const bool v = mine && n > 0;
         const unsigned bm = __ballot_sync(kFull, v);
         const uint32_t cnt = __popc(bm);
@@ -245,9 +267,21 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
     uint32_t *sp = w.spill + (size_t)(blockIdx.x * kWarps + (tid >> 5)) * w.spill_cap * F;
     __shared__ uint32_t s_gw[lane::kGwMax];
     __shared__ uint32_t s_pref[bfs::kStripes + 1];
+    __shared__ uint32_t s_np[lane::kGwMax / 32];  // bit g: a child of group g needs P (NODE_NEEDP)
     for (uint32_t i = tid; i < p.n_nodes; i += kWB) s_nodes[i] = p.nodes[i];
     for (uint32_t i = tid; i < p.n_groups; i += kWB) s_groups[i] = p.groups[i];
     for (uint32_t i = tid; i < p.n_groups && i < lane::kGwMax; i += kWB) s_gw[i] = w.gwant[i];
+    if (tid < lane::kGwMax / 32) s_np[tid] = 0;
+    __syncthreads();
+    for (uint32_t g = tid; g < p.n_groups && g < lane::kGwMax; g += kWB) {
+        const DGroup G = p.groups[g];
+        bool np = false;
+        for (uint32_t ch = G.child_begin; ch < G.child_end; ch++) {
+            const lane::LNode dn = p.nodes[ch];
+            np = np || ((dn.flags & NODE_INNER) && (dn.flags & NODE_NEEDP));
+        }
+        if (np) atomicOr(&s_np[g >> 5], 1u << (g & 31));
+    }
     for (uint32_t i = tid; i < p.n_slots; i += kWB) s_tot[i] = 0;
     if (s_cnt)
         for (uint32_t i = 0; i < p.n_slots; i++) s_cnt[i * kWB + tid] = 0;
@@ -291,6 +325,7 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
 
         bfs::PM<MAXV> x;   // this lane's new partial match: an item, or a child found this round
         bool has = false;
+        uint32_t c_lo = 0, c_end = 0;  // a child's continuation window on its parent's list
         if (top == 0 && sp_top > 0) {
             // ---- the stack ran empty: bring back the most recently spilled pieces (depth first)
             const uint32_t m = min(sp_top, (uint32_t)CAP / 2);
@@ -353,7 +388,8 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
             bool valid = false;
             if (act) {
                 const uint32_t g = stk[0 * CAP + pi];
-                const uint32_t pos = stk[1 * CAP + pi] + at;
+                const uint32_t p0 = stk[1 * CAP + pi];
+                const uint32_t pos = p0 + at;
                 const uint32_t tp = stk[3 * CAP + pi];
                 const uint32_t h = stk[4 * CAP + pi];
                 uint32_t m2g[MAXV];
@@ -361,19 +397,24 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
                 for (int k = 0; k < MAXV; k++) m2g[k] = stk[(6 + k) * CAP + pi];
                 const DGroup G = s_groups[g];
                 const bool glob = GEN && G.kind == ANCHOR_GLOBAL;
+                // successor pointers of the entry's edge, loaded with the entry (no extra round
+                // trip) when a child of this group locates a window from them
+                const bool needp = G.n_inner && (g >= lane::kGwMax || ((s_np[g >> 5] >> (g & 31)) & 1u));
                 uint32_t etr, e1, e2 = 0;
                 uint4 P = make_uint4(0, 0, 0, 0);
                 if (glob) {
                     etr = __ldg(p.tr + pos);
                     e1 = __ldg(p.src + pos);
                     e2 = __ldg(p.dst + pos);
-                    if (G.n_inner) P = __ldg(p.eptr + pos);
+                    if (needp) P = __ldg(p.eptr + pos);
                 } else {
                     const bool out = G.kind == ANCHOR_OUT;
                     const uint2 e = __ldg((out ? p.out_ent : p.in_ent) + pos);
                     etr = e.x;
                     e1 = e.y;
-                    if (G.n_inner) P = __ldg((out ? p.out_ptr : p.in_ptr) + pos);  // with the entry
+                    if (needp) P = __ldg((out ? p.out_ptr : p.in_ptr) + pos);
+                    c_lo = pos + 1;
+                    c_end = p0 + stk[2 * CAP + pi];
                 }
                 valid = etr > tp && etr <= h;
                 uint32_t cls;
@@ -431,7 +472,8 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
             __syncwarp();
         }
         // ---- the new partial matches' windows go on top of the stack (depth first)
-        if (__any_sync(kFull, has)) open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, has, x, c);
+        if (__any_sync(kFull, has))
+            open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, has, x, c_lo, c_end, c);
     }
 
     // ---- counters: lanes -> block -> global, once per block

@@ -196,7 +196,8 @@ __device__ __noinline__ void reload(uint32_t *stk, uint32_t m, const uint32_t *s
 template <int MAXV, bool GEN, int CAP, bool STATS>
 __device__ __forceinline__ void open_push(const WParams &w, const lane::LNode *s_nodes, const DGroup *s_groups,
                                           uint32_t *stk, uint32_t &ps, uint32_t *sp, uint32_t &sp_top, bool has,
-                                          const bfs::PM<MAXV> &x, uint32_t c_lo, uint32_t c_end, bfs::Ctx &c) {
+                                          const bfs::PM<MAXV> &x, uint32_t c_lo, uint32_t c_end, bool c_out,
+                                          bfs::Ctx &c) {
     const bfs::BParams &p = w.b;
     const uint32_t lane_id = threadIdx.x & 31;
     uint32_t gb = 0, ng = 0, same = 0;
@@ -241,7 +242,10 @@ __device__ __forceinline__ void open_push(const WParams &w, const lane::LNode *s
                 for (int k = 0; k < MAXV; k++) stk[(6 + k) * CAP + slot] = x.m2g[k];
             } else {
                 atomicAdd(p.fallback, 1u);
-                bfs::dfs<MAXV, false>(p, s_nodes, s_groups, x, c, gb + q);
+                bfs::PM<MAXV> y = x;
+                if (c_end)  // a child: its successor pointers may not have been loaded with the entry
+                    y.P = __ldg((c_out ? p.out_ptr : p.in_ptr) + (c_lo - 1));
+                bfs::dfs<MAXV, false>(p, s_nodes, s_groups, y, c, gb + q);
                 fell = true;
             }
         }
@@ -326,6 +330,7 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
         bfs::PM<MAXV> x;   // this lane's new partial match: an item, or a child found this round
         bool has = false;
         uint32_t c_lo = 0, c_end = 0;  // a child's continuation window on its parent's list
+        bool c_out = false;
         if (top == 0 && sp_top > 0) {
             // ---- the stack ran empty: bring back the most recently spilled pieces (depth first)
             const uint32_t m = min(sp_top, (uint32_t)CAP / 2);
@@ -415,6 +420,7 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
                     if (needp) P = __ldg((out ? p.out_ptr : p.in_ptr) + pos);
                     c_lo = pos + 1;
                     c_end = p0 + stk[2 * CAP + pi];
+                    c_out = out;
                 }
                 valid = etr > tp && etr <= h;
                 uint32_t cls;
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
         }
         // ---- the new partial matches' windows go on top of the stack (depth first)
         if (__any_sync(kFull, has))
-            open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, has, x, c_lo, c_end, c);
+            open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, has, x, c_lo, c_end, c_out, c);
     }
 
     // ---- counters: lanes -> block -> global, once per block

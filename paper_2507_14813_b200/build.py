@@ -29,20 +29,25 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, ptxas_verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, ptxas_verbose: bool = False, variant: str = "", defines=()) -> str:
+    """variant: build lib/libmayura_<variant>.so with extra -D defines (A/B builds, loaded through
+    MAYURA_LIB_PATH); the default library is lib/libmayura.so."""
+    lib = LIB if not variant else os.path.join(os.path.dirname(LIB), "libmayura_%s.so" % variant)
+    if not variant and not force and not _stale():
         return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    tmp = LIB + ".tmp%d" % os.getpid()
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    tmp = lib + ".tmp%d" % os.getpid()
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O3,-pthread",
+           *["-D" + d for d in defines],
            "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources(), "-lpthread"]
     if ptxas_verbose:
         cmd[1:1] = ["-Xptxas", "-v"]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, ptxas_verbose="--ptxas-v" in sys.argv)
-    print(LIB)
+    var = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else ""
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, ptxas_verbose="--ptxas-v" in sys.argv, variant=var, defines=defs))

@@ -31,9 +31,13 @@
 
 namespace wdfs {
 
+#ifndef WDFS_MINB
+#define WDFS_MINB 6  // resident blocks per SM the register allocation targets (80 registers)
+#endif
+
 constexpr int kWB = 128;                 // threads per block
 constexpr int kWarps = kWB / 32;
-constexpr int kCap = 96;                 // pieces per warp stack in shared memory
+constexpr int kCap = 128;                // pieces per warp stack in shared memory
 constexpr int kCapSmall = 64;            // test instance (MAYURA_WDFS_SMALL=1): spills early and often
 constexpr uint8_t NODE_NEEDP = 16;       // LNode flag: a group of the node needs its edge's successor
                                          // pointers (a START_P* group that is not a same-list continuation)
@@ -65,7 +69,7 @@ __host__ __device__ inline size_t off_stk(uint32_t nn, uint32_t ng, uint32_t ns,
     return lane::align16(off_cnt(nn, ng, ns) + (lanecnt ? (size_t)ns * kWB * 4 : 0));
 }
 __host__ __device__ inline size_t smem_bytes(uint32_t nn, uint32_t ng, uint32_t ns, bool lanecnt, int maxv, int cap) {
-    return off_stk(nn, ng, ns, lanecnt) + (size_t)kWarps * ((6 + maxv) * cap + (10 + maxv) * 32) * 4;
+    return off_stk(nn, ng, ns, lanecnt) + (size_t)kWarps * (6 + maxv) * cap * 4;
 }
 
 // Length of a window: entries [lo, lo + n) are the entries of list `ent` from lo with time
@@ -186,61 +190,23 @@ __device__ __noinline__ void reload(uint32_t *stk, uint32_t m, const uint32_t *s
     __syncwarp();
 }
 
-// Per-warp staging area (shared memory, SoA, 32 slots = one per lane) of the partial matches to
-// expand at the next step: children found by the last round, or items just taken.  Words:
-template <int MAXV>
-struct Stage {
-    // 0 node | c_out << 31, 1 tr_prev, 2 h, 3 root, 4..7 P, 8 c_lo, 9 c_end, 10.. m2g[MAXV]
-    static constexpr int F = 10 + MAXV;
-};
-
-template <int MAXV>
-__device__ __forceinline__ void stage_put(uint32_t *sg, uint32_t lane, const bfs::PM<MAXV> &x, uint32_t c_lo,
-                                          uint32_t c_end, bool c_out) {
-    sg[0 * 32 + lane] = x.node | (c_out ? 0x80000000u : 0u);
-    sg[1 * 32 + lane] = x.tr_prev;
-    sg[2 * 32 + lane] = x.h;
-    sg[3 * 32 + lane] = x.root;
-    sg[4 * 32 + lane] = x.P.x;
-    sg[5 * 32 + lane] = x.P.y;
-    sg[6 * 32 + lane] = x.P.z;
-    sg[7 * 32 + lane] = x.P.w;
-    sg[8 * 32 + lane] = c_lo;
-    sg[9 * 32 + lane] = c_end;
-#pragma unroll
-    for (int k = 0; k < MAXV; k++) sg[(10 + k) * 32 + lane] = x.m2g[k];
-}
-
-// Warp-collective: every lane with a staged partial match locates the windows of its anchor
-// groups and pushes the non-empty ones on the warp's stack (warp-aggregated).  A full stack
-// spills its bottom half to global memory; a full spill area makes the lane mine the partial
-// match from that group on depth-first itself (exact; counted in p.fallback).
+// Warp-collective: every lane with `has` locates the windows of x's anchor groups and pushes the
+// non-empty ones on the warp's stack (warp-aggregated).  A full stack spills its bottom half to
+// global memory; a full spill area makes the lane mine x from that group on depth-first itself
+// (exact; counted in p.fallback).
 // A child matched at list position c_lo - 1 of its parent's window [.., c_end) continues on the
 // same list in every group flagged in its node's `same` mask: that window is [c_lo, c_end), no
-// memory access needed (items pass c_end = 0: no continuation).
+// memory access needed (items from a global cursor pass c_end = 0: no continuation).
 template <int MAXV, bool GEN, int CAP, bool STATS>
 __device__ __forceinline__ void open_push(const WParams &w, const lane::LNode *s_nodes, const DGroup *s_groups,
-                                          uint32_t *stk, uint32_t &ps, uint32_t *sp, uint32_t &sp_top,
-                                          const uint32_t *sg, bool has, bfs::Ctx &c) {
+                                          uint32_t *stk, uint32_t &ps, uint32_t *sp, uint32_t &sp_top, bool has,
+                                          const bfs::PM<MAXV> &x, uint32_t c_lo, uint32_t c_end, bool c_out,
+                                          uint32_t *my_cnt, unsigned long long *s_tot, unsigned long long *st) {
     const bfs::BParams &p = w.b;
     const uint32_t lane_id = threadIdx.x & 31;
-    bfs::PM<MAXV> x;
-    uint32_t gb = 0, ng = 0, same = 0, c_lo = 0, c_end = 0;
-    bool c_out = false;
+    uint32_t gb = 0, ng = 0, same = 0;
     if (has) {
-        const uint32_t w0 = sg[0 * 32 + lane_id];
-        x.node = w0 & 0xFFFFu;
-        c_out = (w0 >> 31) != 0;
-        x.tr_prev = sg[1 * 32 + lane_id];
-        x.h = sg[2 * 32 + lane_id];
-        x.root = sg[3 * 32 + lane_id];
-        x.P = make_uint4(sg[4 * 32 + lane_id], sg[5 * 32 + lane_id], sg[6 * 32 + lane_id], sg[7 * 32 + lane_id]);
-        c_lo = sg[8 * 32 + lane_id];
-        c_end = sg[9 * 32 + lane_id];
-#pragma unroll
-        for (int k = 0; k < MAXV; k++) x.m2g[k] = sg[(10 + k) * 32 + lane_id];
         const lane::LNode xn = s_nodes[x.node];
-        x.nv = xn.nv;
         gb = xn.group_begin;
         ng = xn.group_end - xn.group_begin;
         same = c_end ? xn.same : 0u;
@@ -262,11 +228,10 @@ __device__ __forceinline__ void open_push(const WParams &w, const lane::LNode *s
         const unsigned bm = __ballot_sync(kFull, v);
         const uint32_t cnt = __popc(bm);
         if (ps + cnt > CAP && ps >= 2 && sp_top + ps / 2 <= w.spill_cap) {
-            const uint32_t m = ps / 2;
-            spill_bottom<MAXV, CAP>(stk, ps, m, sp, sp_top);
-            sp_top += m;
-            ps -= m;
-            if (STATS && lane_id == 0) c.st[ST_OFFLOADS]++;
+            spill_bottom<MAXV, CAP>(stk, ps, ps / 2, sp, sp_top);
+            sp_top += ps / 2;
+            ps -= ps / 2;
+            if (STATS && lane_id == 0) st[ST_OFFLOADS]++;
         }
         const uint32_t slot = ps + __popc(bm & ((1u << lane_id) - 1u));
         if (v) {
@@ -284,27 +249,23 @@ __device__ __forceinline__ void open_push(const WParams &w, const lane::LNode *s
                 bfs::PM<MAXV> y = x;
                 if (c_end)  // a child: its successor pointers may not have been loaded with the entry
                     y.P = __ldg((c_out ? p.out_ptr : p.in_ptr) + (c_lo - 1));
+                bfs::Ctx c;  // built here only: a Ctx whose address escapes lives in local memory
+                c.cnt = my_cnt;
+                c.stride = kWB;
+                c.tot = s_tot;
+                c.em_next = c.em_end = 0;
                 bfs::dfs<MAXV, false>(p, s_nodes, s_groups, y, c, gb + q);
                 fell = true;
             }
         }
         ps = min(ps + cnt, (uint32_t)CAP);
-        if (STATS && lane_id == 0) c.st[ST_WINDOWS] += cnt;
+        if (STATS && lane_id == 0) st[ST_WINDOWS] += cnt;
     }
     __syncwarp();
 }
 
-// One iteration of a warp (software-pipelined by one round):
-//   (a) select this round's entries (one per lane) from the live pieces at the top of the stack
-//       and issue their loads; the pieces are consumed in place (pos += taken, n -= taken), a piece
-//       at n = 0 is garbage until it surfaces at the top and is popped;
-//   (b) while those loads are in flight, expand the staged partial matches of the previous round
-//       (window location probes overlap the entry loads) and push their pieces on top;
-//   (c) test the entries: count completions, stage the inner hits for the next iteration.
-// When fewer than 32 candidates are stacked, free staging slots take the next items (partial
-// matches of the breadth-first level, light roots, or root edges) from a global cursor.
 template <int MAXV, bool GEN, int CAP, bool STATS>
-__global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WParams w) {
+__global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_constant__ WParams w) {
     pdl_begin();
     const bfs::BParams &p = w.b;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -314,14 +275,12 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
         smem + lane::align16((size_t)p.n_nodes * sizeof(lane::LNode)) + lane::align16((size_t)p.n_groups * sizeof(DGroup)));
     uint32_t *s_cnt = w.lanecnt ? reinterpret_cast<uint32_t *>(smem + w.o_cnt) : nullptr;
     const uint32_t tid = threadIdx.x, lane_id = tid & 31;
-    constexpr int F = Piece<MAXV>::F, SF = Stage<MAXV>::F;
-    uint32_t *stk = reinterpret_cast<uint32_t *>(smem + w.o_stk) + (size_t)(tid >> 5) * (F * CAP + SF * 32);
-    uint32_t *sg = stk + F * CAP;
+    constexpr int F = Piece<MAXV>::F;
+    uint32_t *stk = reinterpret_cast<uint32_t *>(smem + w.o_stk) + (size_t)(tid >> 5) * F * CAP;
     uint32_t *sp = w.spill + (size_t)(blockIdx.x * kWarps + (tid >> 5)) * w.spill_cap * F;
     __shared__ uint32_t s_gw[lane::kGwMax];
     __shared__ uint32_t s_pref[bfs::kStripes + 1];
     __shared__ uint32_t s_np[lane::kGwMax / 32];  // bit g: a child of group g needs P (NODE_NEEDP)
-    __shared__ uint32_t s_own[kWarps][32];        // per warp: round slot -> lane of the piece starting there
     for (uint32_t i = tid; i < p.n_nodes; i += kWB) s_nodes[i] = p.nodes[i];
     for (uint32_t i = tid; i < p.n_groups; i += kWB) s_groups[i] = p.groups[i];
     for (uint32_t i = tid; i < p.n_groups && i < lane::kGwMax; i += kWB) s_gw[i] = w.gwant[i];
@@ -349,44 +308,39 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
     }
     __syncthreads();
 
-    bfs::Ctx c;
-    c.cnt = s_cnt ? s_cnt + tid : nullptr;
-    c.stride = kWB;
-    c.tot = s_tot;
+    // completion counters: this lane's u32 per slot (flushed to the block's u64 before 2^31), or
+    // block u64 atomics when the group has too many slots (kept in registers, not in a bfs::Ctx:
+    // the fallback passes one by address, which would put it in local memory)
+    uint32_t *const my_cnt = s_cnt ? s_cnt + tid : nullptr;
+    auto cnt_add = [&](uint32_t slot) {
+        if (my_cnt) {
+            uint32_t *q = my_cnt + slot * kWB;
+            uint32_t v = *q + 1;
+            if (v >= 0x80000000u) {
+                atomicAdd(&s_tot[slot], (unsigned long long)v);
+                v = 0;
+            }
+            *q = v;
+        } else {
+            atomicAdd(&s_tot[slot], 1ull);
+        }
+    };
+    unsigned long long st[ST_N];
 #pragma unroll
-    for (int i = 0; i < ST_N; i++) c.st[i] = 0;
-    c.em_next = c.em_end = 0;
+    for (int i = 0; i < ST_N; i++) st[i] = 0;
 
     const lane::LNode root = s_nodes[0];
     const uint32_t n_pm = s_pref[bfs::kStripes];
     const uint32_t n_items = w.direct ? p.n_roots : n_pm + (p.light ? *(volatile const uint32_t *)p.light_cnt : 0u);
-    const unsigned lt = (1u << lane_id) - 1u;
 
-    uint32_t ps = 0;           // warp-uniform stack height in shared memory (garbage pieces included)
+    uint32_t ps = 0;           // warp-uniform stack height (shared memory)
     uint32_t sp_top = 0;       // warp-uniform spilled pieces (global memory)
     uint32_t cb = 0, cl = 0;   // warp-uniform item chunk
     bool items_left = true;
-    bool staged = false;       // this lane's staging slot holds a partial match to expand
     for (;;) {
-        // ---- pop the garbage (consumed pieces) at the top
-        uint32_t pn;
-        for (;;) {
-            pn = lane_id < ps ? stk[2 * CAP + ps - 1 - lane_id] : 1u;
-            const unsigned dead = __ballot_sync(kFull, pn == 0);
-            const uint32_t run = ~dead ? (uint32_t)__ffs(~dead) - 1u : 32u;  // leading n = 0 pieces
-            if (run == 0) break;
-            ps -= run;
-        }
-        if (ps == 0 && sp_top > 0) {  // the stack ran empty: bring back the last spilled pieces
-            const uint32_t m = min(sp_top, (uint32_t)CAP / 2);
-            reload<MAXV, CAP>(stk, m, sp, sp_top);
-            sp_top -= m;
-            ps = m;
-            if (STATS && lane_id == 0) c.st[ST_CONTEXTS]++;
-            continue;
-        }
+        // ---- the top pieces: candidate counts and their running sum (top first)
         const uint32_t top = ps;
-        if (lane_id >= top) pn = 0;
+        const uint32_t pn = lane_id < top ? stk[2 * CAP + top - 1 - lane_id] : 0u;
         uint32_t incl = pn;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -395,169 +349,159 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
         }
         const uint32_t tot = __shfl_sync(kFull, incl, 31);
 
-        // ---- fewer than 32 candidates stacked: free staging slots take the next items
+        bfs::PM<MAXV> x;   // this lane's new partial match: an item, or a child found this round
+        bool has = false;
+        uint32_t c_lo = 0, c_end = 0;  // a child's continuation window on its parent's list
+        bool c_out = false;
+        if (top == 0 && sp_top > 0) {
+            // ---- the stack ran empty: bring back the most recently spilled pieces (depth first)
+            const uint32_t m = min(sp_top, (uint32_t)CAP / 2);
+            reload<MAXV, CAP>(stk, m, sp, sp_top);
+            sp_top -= m;
+            ps = m;
+            if (STATS && lane_id == 0) st[ST_CONTEXTS]++;
+            continue;
+        }
         if (tot < 32 && items_left && sp_top == 0) {
-            const unsigned fr = __ballot_sync(kFull, !staged);
-            const uint32_t nfree = __popc(fr);
-            uint32_t taken = 0;
-            while (taken < nfree && items_left) {
-                if (cl == 0) {
-                    uint32_t b = 0, sz = 0;
-                    if (lane_id == 0) {
-                        const uint32_t cur = *(volatile uint32_t *)w.lb;
-                        const uint32_t rem = cur < n_items ? n_items - cur : 0u;
-                        sz = max(32u, min(256u, (rem / (4u * gridDim.x * kWarps)) & ~31u));
-                        b = atomicAdd(w.lb, sz);
-                    }
-                    b = __shfl_sync(kFull, b, 0);
-                    sz = __shfl_sync(kFull, sz, 0);
-                    if (b >= n_items) {
-                        items_left = false;
-                        break;
-                    }
-                    cb = b;
-                    cl = min(sz, n_items - b);
+            // ---- fewer than 32 candidates stacked: take the next items (one per lane)
+            if (cl == 0) {
+                uint32_t b = 0, sz = 0;
+                if (lane_id == 0) {
+                    const uint32_t cur = *(volatile uint32_t *)w.lb;
+                    const uint32_t rem = cur < n_items ? n_items - cur : 0u;
+                    sz = max(32u, min(256u, (rem / (4u * gridDim.x * kWarps)) & ~31u));
+                    b = atomicAdd(w.lb, sz);
                 }
-                const uint32_t take = min(nfree - taken, cl);
-                const uint32_t rank = __popc(fr & lt);
-                if (!staged && rank >= taken && rank < taken + take) {
-                    const uint32_t item = cb + (rank - taken);
-                    bfs::PM<MAXV> x;
-                    bool has = false;
-                    if (w.direct) {  // a root edge: count the root node's completion, expand it if inner
-                        const uint32_t r = p.r0 + item;
-                        if (bfs::load_root<MAXV>(p, r, x)) {
-                            if (root.flags & NODE_COMPLETION) bfs::count_add(c, root.slot, 1);
-                            has = (root.flags & NODE_INNER) != 0;
+                b = __shfl_sync(kFull, b, 0);
+                sz = __shfl_sync(kFull, sz, 0);
+                if (b >= n_items) {
+                    items_left = false;
+                    continue;
+                }
+                cb = b;
+                cl = min(sz, n_items - b);
+            }
+            const uint32_t take = min(32u, cl);
+            const uint32_t item = cb + lane_id;
+            cb += take;
+            cl -= take;
+            if (lane_id < take) {
+                if (w.direct) {  // a root edge: count the root node's completion, expand it if inner
+                    const uint32_t r = p.r0 + item;
+                    if (bfs::load_root<MAXV>(p, r, x)) {
+                        if (root.flags & NODE_COMPLETION) cnt_add(root.slot);
+                        has = (root.flags & NODE_INNER) != 0;
+                    }
+                } else if (item < n_pm) {  // a partial match of the breadth-first level (counted there)
+                    bfs::load_rec<MAXV>(p, s_pref, item, x);
+                    has = x.node != bfs::kHole;
+                } else {  // a light root (its completion was counted by the breadth-first level)
+                    has = bfs::load_root<MAXV>(p, __ldg(p.light + (item - n_pm)), x);
+                }
+            }
+            if (STATS && lane_id == 0) st[ST_ROOTS] += take;
+        } else {
+            if (top == 0) break;  // no items left, nothing stacked or spilled
+            // ---- this round: T entries, one per lane, from the top pieces (the last one possibly split)
+            const uint32_t T = min(tot, 32u);
+            const uint32_t excl = incl - pn;
+            const bool pc = lane_id < top && excl < T;  // this piece contributes entries
+            const uint32_t smask = __reduce_or_sync(kFull, pc ? (1u << excl) : 0u);
+            const uint32_t kf = __popc(__ballot_sync(kFull, lane_id < top && incl <= T));  // taken whole
+            const bool act = lane_id < T;
+            const uint32_t upto = smask & ((2u << lane_id) - 1u);
+            const uint32_t pi = top - 1 - (act ? (uint32_t)__popc(upto) - 1u : 0u);  // this lane's piece
+            const uint32_t at = lane_id - (31 - __clz(upto | 1u));                    // offset in the piece
+            bool valid = false;
+            if (act) {
+                const uint32_t g = stk[0 * CAP + pi];
+                const uint32_t p0 = stk[1 * CAP + pi];
+                const uint32_t pos = p0 + at;
+                const uint32_t tp = stk[3 * CAP + pi];
+                const uint32_t h = stk[4 * CAP + pi];
+                uint32_t m2g[MAXV];
+#pragma unroll
+                for (int k = 0; k < MAXV; k++) m2g[k] = stk[(6 + k) * CAP + pi];
+                const DGroup G = s_groups[g];
+                const bool glob = GEN && G.kind == ANCHOR_GLOBAL;
+                // successor pointers of the entry's edge, loaded with the entry (no extra round
+                // trip) when a child of this group locates a window from them
+                const bool needp = G.n_inner && (g >= lane::kGwMax || ((s_np[g >> 5] >> (g & 31)) & 1u));
+                uint32_t etr, e1, e2 = 0;
+                uint4 P = make_uint4(0, 0, 0, 0);
+                if (glob) {
+                    etr = __ldg(p.tr + pos);
+                    e1 = __ldg(p.src + pos);
+                    e2 = __ldg(p.dst + pos);
+                    if (needp) P = __ldg(p.eptr + pos);
+                } else {
+                    const bool out = G.kind == ANCHOR_OUT;
+                    const uint2 e = __ldg((out ? p.out_ent : p.in_ent) + pos);
+                    etr = e.x;
+                    e1 = e.y;
+                    if (needp) P = __ldg((out ? p.out_ptr : p.in_ptr) + pos);
+                    c_lo = pos + 1;
+                    c_end = p0 + stk[2 * CAP + pi];
+                    c_out = out;
+                }
+                valid = etr > tp && etr <= h;
+                uint32_t cls;
+                if (glob)
+                    cls = (e1 != e2 && lane::classify<MAXV>(m2g, e1) == CLS_NEW &&
+                           lane::classify<MAXV>(m2g, e2) == CLS_NEW) ? CLS_NEW : 0xFEu;
+                else
+                    cls = lane::classify<MAXV>(m2g, e1);
+                uint32_t hit = kNone;
+                if (G.child_end - G.child_begin <= 4 && g < lane::kGwMax) {
+                    const uint32_t eq = __vcmpeq4(s_gw[g], cls * 0x01010101u);
+                    hit = eq ? G.child_begin + ((__ffs(eq) - 1) >> 3) : kNone;
+                } else {
+                    hit = bfs::find_child(s_nodes, G, cls);
+                }
+                if (valid && hit != kNone) {
+                    const lane::LNode dn = s_nodes[hit];
+                    if (dn.flags & NODE_COMPLETION) cnt_add(dn.slot);
+                    if (STATS) st[ST_MATCHES] += (dn.flags & NODE_COMPLETION) ? 1 : 0;
+                    if (dn.flags & NODE_INNER) {  // the child partial match (Algo 3 l.665-669)
+                        has = true;
+#pragma unroll
+                        for (int k = 0; k < MAXV; k++) x.m2g[k] = m2g[k];
+                        if (dn.n_new == 2) {
+                            lane::m2g_set<MAXV>(x.m2g, dn.nv - 2u, e1);
+                            lane::m2g_set<MAXV>(x.m2g, dn.nv - 1u, e2);
+                        } else if (dn.n_new == 1) {
+                            lane::m2g_set<MAXV>(x.m2g, dn.nv - 1u, e1);
                         }
-                    } else if (item < n_pm) {  // a partial match of the breadth-first level (counted there)
-                        bfs::load_rec<MAXV>(p, s_pref, item, x);
-                        has = x.node != bfs::kHole;
-                    } else {  // a light root (its completion was counted by the breadth-first level)
-                        has = bfs::load_root<MAXV>(p, __ldg(p.light + (item - n_pm)), x);
+                        x.node = hit;
+                        x.nv = dn.nv;
+                        x.tr_prev = etr;
+                        x.h = h;
+                        x.root = stk[5 * CAP + pi];
+                        x.P = P;
+                        if (STATS) st[ST_NODES]++;
                     }
-                    if (has) stage_put<MAXV>(sg, lane_id, x, 0u, 0u, false);
-                    staged = has;
                 }
-                cb += take;
-                cl -= take;
-                taken += take;
-                if (STATS && lane_id == 0) c.st[ST_ROOTS] += take;
+            }
+            if (STATS) {
+                const uint32_t nv = __popc(__ballot_sync(kFull, valid));
+                if (lane_id == 0) {
+                    st[ST_BATCHES]++;
+                    st[ST_PROBES] += T;
+                    st[ST_ENTRIES] += nv;
+                }
             }
             __syncwarp();
-        }
-        if (top == 0 && sp_top == 0 && !items_left && !__any_sync(kFull, staged)) break;
-
-        // ---- (a) this round's entries: T, one per lane, from the live top pieces
-        const uint32_t T = min(tot, 32u);
-        const uint32_t excl = incl - pn;
-        const bool pc = pn > 0 && excl < T;  // this piece contributes entries
-        const uint32_t smask = __reduce_or_sync(kFull, pc ? (1u << excl) : 0u);
-        if (pc) s_own[tid >> 5][excl] = lane_id;  // slot excl starts the piece of this lane
-        __syncwarp();
-        const bool act = lane_id < T;
-        const uint32_t st0 = 31 - __clz((smask & ((2u << lane_id) - 1u)) | 1u);  // first slot of my piece
-        const uint32_t pi = top - 1 - (act ? s_own[tid >> 5][st0] : 0u);
-        const uint32_t at = lane_id - st0;                                           // offset in the piece
-        // everything the test needs is read now: the pushes of step (b) may spill or overwrite
-        uint32_t g = 0, pos = 0, c_end = 0, etr = 0, e1 = 0, e2 = 0, tp = 0, h = 0, rt = 0;
-        uint32_t m2g[MAXV];
-        uint4 P = make_uint4(0, 0, 0, 0);
-        bool glob = false, out = false;
-        if (act) {
-            tp = stk[3 * CAP + pi];
-            h = stk[4 * CAP + pi];
-            rt = stk[5 * CAP + pi];
-#pragma unroll
-            for (int k = 0; k < MAXV; k++) m2g[k] = stk[(6 + k) * CAP + pi];
-            g = stk[0 * CAP + pi];
-            const uint32_t p0 = stk[1 * CAP + pi];
-            pos = p0 + at;
-            c_end = p0 + stk[2 * CAP + pi];
-            const DGroup G = s_groups[g];
-            glob = GEN && G.kind == ANCHOR_GLOBAL;
-            out = G.kind == ANCHOR_OUT;
-            // successor pointers of the entry's edge, loaded with the entry (no extra round trip)
-            // when a child of this group locates a window from them
-            const bool needp = G.n_inner && (g >= lane::kGwMax || ((s_np[g >> 5] >> (g & 31)) & 1u));
-            if (glob) {
-                etr = __ldg(p.tr + pos);
-                e1 = __ldg(p.src + pos);
-                e2 = __ldg(p.dst + pos);
-                if (needp) P = __ldg(p.eptr + pos);
-            } else {
-                const uint2 e = __ldg((out ? p.out_ent : p.in_ent) + pos);
-                etr = e.x;
-                e1 = e.y;
-                if (needp) P = __ldg((out ? p.out_ptr : p.in_ptr) + pos);
+            // ---- pop the pieces taken whole; advance the split one
+            if (lane_id == kf && kf < top && excl < T) {
+                stk[1 * CAP + top - 1 - kf] += T - excl;
+                stk[2 * CAP + top - 1 - kf] -= T - excl;
             }
+            ps = top - kf;
+            __syncwarp();
         }
-        __syncwarp();
-        if (pc) {  // consume in place (the piece's lane)
-            const uint32_t taken = min(pn, T - excl);
-            stk[1 * CAP + top - 1 - lane_id] += taken;
-            stk[2 * CAP + top - 1 - lane_id] -= taken;
-        }
-        __syncwarp();
-
-        // ---- (b) expand the staged partial matches while the entries are in flight
-        if (__any_sync(kFull, staged)) {
-            open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, sg, staged, c);
-            staged = false;
-        }
-
-        // ---- (c) test the entries
-        bool valid = false;
-        if (act) {
-            valid = etr > tp && etr <= h;
-            uint32_t cls;
-            if (glob)
-                cls = (e1 != e2 && lane::classify<MAXV>(m2g, e1) == CLS_NEW &&
-                       lane::classify<MAXV>(m2g, e2) == CLS_NEW) ? CLS_NEW : 0xFEu;
-            else
-                cls = lane::classify<MAXV>(m2g, e1);
-            const DGroup G = s_groups[g];
-            uint32_t hit = kNone;
-            if (G.child_end - G.child_begin <= 4 && g < lane::kGwMax) {
-                const uint32_t eq = __vcmpeq4(s_gw[g], cls * 0x01010101u);
-                hit = eq ? G.child_begin + ((__ffs(eq) - 1) >> 3) : kNone;
-            } else {
-                hit = bfs::find_child(s_nodes, G, cls);
-            }
-            if (valid && hit != kNone) {
-                const lane::LNode dn = s_nodes[hit];
-                if (dn.flags & NODE_COMPLETION) bfs::count_add(c, dn.slot, 1);
-                if (STATS) c.st[ST_MATCHES] += (dn.flags & NODE_COMPLETION) ? 1 : 0;
-                if (dn.flags & NODE_INNER) {  // the child partial match (Algo 3 l.665-669), staged
-                    bfs::PM<MAXV> x;
-#pragma unroll
-                    for (int k = 0; k < MAXV; k++) x.m2g[k] = m2g[k];
-                    if (dn.n_new == 2) {
-                        lane::m2g_set<MAXV>(x.m2g, dn.nv - 2u, e1);
-                        lane::m2g_set<MAXV>(x.m2g, dn.nv - 1u, e2);
-                    } else if (dn.n_new == 1) {
-                        lane::m2g_set<MAXV>(x.m2g, dn.nv - 1u, e1);
-                    }
-                    x.node = hit;
-                    x.tr_prev = etr;
-                    x.h = h;
-                    x.root = rt;
-                    x.P = P;
-                    stage_put<MAXV>(sg, lane_id, x, glob ? 0u : pos + 1, glob ? 0u : c_end, out);
-                    staged = true;
-                    if (STATS) c.st[ST_NODES]++;
-                }
-            }
-        }
-        if (STATS) {
-            const uint32_t nv = __popc(__ballot_sync(kFull, valid));
-            if (lane_id == 0 && T) {
-                c.st[ST_BATCHES]++;
-                c.st[ST_PROBES] += T;
-                c.st[ST_ENTRIES] += nv;
-            }
-        }
-        __syncwarp();
+        // ---- the new partial matches' windows go on top of the stack (depth first)
+        if (__any_sync(kFull, has))
+            open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, has, x, c_lo, c_end, c_out, my_cnt, s_tot, st);
     }
 
     // ---- counters: lanes -> block -> global, once per block
@@ -579,7 +523,7 @@ __global__ void __launch_bounds__(kWB, 6) wdfs_kernel(const __grid_constant__ WP
     if (STATS) {
 #pragma unroll
         for (int i = 0; i < ST_N; i++) {
-            unsigned long long v = c.st[i];
+            unsigned long long v = st[i];
 #pragma unroll
             for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
             if (lane_id == 0 && v) atomicAdd(p.stats + i, v);

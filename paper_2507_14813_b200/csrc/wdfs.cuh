@@ -32,7 +32,7 @@
 namespace wdfs {
 
 #ifndef WDFS_MINB
-#define WDFS_MINB 6  // resident blocks per SM the register allocation targets (80 registers)
+#define WDFS_MINB 5  // resident blocks per SM the register allocation targets (96 registers)
 #endif
 
 constexpr int kWB = 128;                 // threads per block
@@ -69,7 +69,7 @@ __host__ __device__ inline size_t off_stk(uint32_t nn, uint32_t ng, uint32_t ns,
     return lane::align16(off_cnt(nn, ng, ns) + (lanecnt ? (size_t)ns * kWB * 4 : 0));
 }
 __host__ __device__ inline size_t smem_bytes(uint32_t nn, uint32_t ng, uint32_t ns, bool lanecnt, int maxv, int cap) {
-    return off_stk(nn, ng, ns, lanecnt) + (size_t)kWarps * (6 + maxv) * cap * 4;
+    return off_stk(nn, ng, ns, lanecnt) + (size_t)kWarps * ((6 + maxv) * cap + (10 + maxv) * 32) * 4;
 }
 
 // Length of a window: entries [lo, lo + n) are the entries of list `ent` from lo with time
@@ -190,6 +190,46 @@ __device__ __noinline__ void reload(uint32_t *stk, uint32_t m, const uint32_t *s
     __syncwarp();
 }
 
+// Per-warp staging area (shared memory, SoA, 32 slots = one per lane) of the children found by a
+// round's second slots, expanded after the first slots' ones.  Words: 0 node | c_out << 31,
+// 1 tr_prev, 2 h, 3 root, 4..7 P, 8 c_lo, 9 c_end, 10.. m2g[MAXV]
+template <int MAXV>
+struct Stage {
+    static constexpr int F = 10 + MAXV;
+};
+template <int MAXV>
+__device__ __forceinline__ void stage_put(uint32_t *sg, uint32_t lane, const bfs::PM<MAXV> &x, uint32_t c_lo,
+                                          uint32_t c_end, bool c_out) {
+    sg[0 * 32 + lane] = x.node | (c_out ? 0x80000000u : 0u);
+    sg[1 * 32 + lane] = x.tr_prev;
+    sg[2 * 32 + lane] = x.h;
+    sg[3 * 32 + lane] = x.root;
+    sg[4 * 32 + lane] = x.P.x;
+    sg[5 * 32 + lane] = x.P.y;
+    sg[6 * 32 + lane] = x.P.z;
+    sg[7 * 32 + lane] = x.P.w;
+    sg[8 * 32 + lane] = c_lo;
+    sg[9 * 32 + lane] = c_end;
+#pragma unroll
+    for (int k = 0; k < MAXV; k++) sg[(10 + k) * 32 + lane] = x.m2g[k];
+}
+template <int MAXV>
+__device__ __forceinline__ void stage_get(const uint32_t *sg, uint32_t lane, bfs::PM<MAXV> &x, uint32_t &c_lo,
+                                          uint32_t &c_end, bool &c_out, const lane::LNode *s_nodes) {
+    const uint32_t w0 = sg[0 * 32 + lane];
+    x.node = w0 & 0xFFFFu;
+    c_out = (w0 >> 31) != 0;
+    x.nv = s_nodes[x.node].nv;
+    x.tr_prev = sg[1 * 32 + lane];
+    x.h = sg[2 * 32 + lane];
+    x.root = sg[3 * 32 + lane];
+    x.P = make_uint4(sg[4 * 32 + lane], sg[5 * 32 + lane], sg[6 * 32 + lane], sg[7 * 32 + lane]);
+    c_lo = sg[8 * 32 + lane];
+    c_end = sg[9 * 32 + lane];
+#pragma unroll
+    for (int k = 0; k < MAXV; k++) x.m2g[k] = sg[(10 + k) * 32 + lane];
+}
+
 // Warp-collective: every lane with `has` locates the windows of x's anchor groups and pushes the
 // non-empty ones on the warp's stack (warp-aggregated).  A full stack spills its bottom half to
 // global memory; a full spill area makes the lane mine x from that group on depth-first itself
@@ -276,11 +316,14 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
     uint32_t *s_cnt = w.lanecnt ? reinterpret_cast<uint32_t *>(smem + w.o_cnt) : nullptr;
     const uint32_t tid = threadIdx.x, lane_id = tid & 31;
     constexpr int F = Piece<MAXV>::F;
-    uint32_t *stk = reinterpret_cast<uint32_t *>(smem + w.o_stk) + (size_t)(tid >> 5) * F * CAP;
+    constexpr int SF = Stage<MAXV>::F;
+    uint32_t *stk = reinterpret_cast<uint32_t *>(smem + w.o_stk) + (size_t)(tid >> 5) * (F * CAP + SF * 32);
+    uint32_t *sg = stk + F * CAP;
     uint32_t *sp = w.spill + (size_t)(blockIdx.x * kWarps + (tid >> 5)) * w.spill_cap * F;
     __shared__ uint32_t s_gw[lane::kGwMax];
     __shared__ uint32_t s_pref[bfs::kStripes + 1];
     __shared__ uint32_t s_np[lane::kGwMax / 32];  // bit g: a child of group g needs P (NODE_NEEDP)
+    __shared__ uint32_t s_own[kWarps][64];        // per warp: round slot -> index of the piece starting there
     for (uint32_t i = tid; i < p.n_nodes; i += kWB) s_nodes[i] = p.nodes[i];
     for (uint32_t i = tid; i < p.n_groups; i += kWB) s_groups[i] = p.groups[i];
     for (uint32_t i = tid; i < p.n_groups && i < lane::kGwMax; i += kWB) s_gw[i] = w.gwant[i];
@@ -337,20 +380,104 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
     uint32_t sp_top = 0;       // warp-uniform spilled pieces (global memory)
     uint32_t cb = 0, cl = 0;   // warp-uniform item chunk
     bool items_left = true;
+    uint32_t *own = s_own[tid >> 5];
+    uint32_t *sgb = sg;  // staging of the second slot's children
+
+    // Test the candidate entry of one slot: window entry `at` of piece `pi`.  Completions are
+    // counted; an inner hit fills y (the child partial match) and its continuation window.
+    auto test_slot = [&](uint32_t pi, uint32_t at, bfs::PM<MAXV> &y, uint32_t &y_lo, uint32_t &y_end,
+                         bool &y_out) -> bool {
+        const uint32_t g = stk[0 * CAP + pi];
+        const uint32_t p0 = stk[1 * CAP + pi];
+        const uint32_t pos = p0 + at;
+        const uint32_t tp = stk[3 * CAP + pi];
+        const uint32_t h = stk[4 * CAP + pi];
+        const DGroup G = s_groups[g];
+        const bool glob = GEN && G.kind == ANCHOR_GLOBAL;
+        // successor pointers of the entry's edge, loaded with the entry (no extra round trip)
+        // when a child of this group locates a window from them
+        const bool needp = G.n_inner && (g >= lane::kGwMax || ((s_np[g >> 5] >> (g & 31)) & 1u));
+        uint32_t etr, e1, e2 = 0;
+        uint4 P = make_uint4(0, 0, 0, 0);
+        const bool out = G.kind == ANCHOR_OUT;
+        if (glob) {
+            etr = __ldg(p.tr + pos);
+            e1 = __ldg(p.src + pos);
+            e2 = __ldg(p.dst + pos);
+            if (needp) P = __ldg(p.eptr + pos);
+        } else {
+            const uint2 e = __ldg((out ? p.out_ent : p.in_ent) + pos);
+            etr = e.x;
+            e1 = e.y;
+            if (needp) P = __ldg((out ? p.out_ptr : p.in_ptr) + pos);
+        }
+        uint32_t m2g[MAXV];
+#pragma unroll
+        for (int k = 0; k < MAXV; k++) m2g[k] = stk[(6 + k) * CAP + pi];
+        const bool valid = etr > tp && etr <= h;
+        if (STATS) st[ST_ENTRIES] += valid ? 1 : 0;
+        uint32_t cls;
+        if (glob)
+            cls = (e1 != e2 && lane::classify<MAXV>(m2g, e1) == CLS_NEW &&
+                   lane::classify<MAXV>(m2g, e2) == CLS_NEW) ? CLS_NEW : 0xFEu;
+        else
+            cls = lane::classify<MAXV>(m2g, e1);
+        uint32_t hit = kNone;
+        if (G.child_end - G.child_begin <= 4 && g < lane::kGwMax) {
+            const uint32_t eq = __vcmpeq4(s_gw[g], cls * 0x01010101u);
+            hit = eq ? G.child_begin + ((__ffs(eq) - 1) >> 3) : kNone;
+        } else {
+            hit = bfs::find_child(s_nodes, G, cls);
+        }
+        if (!valid || hit == kNone) return false;
+        const lane::LNode dn = s_nodes[hit];
+        if (dn.flags & NODE_COMPLETION) cnt_add(dn.slot);
+        if (STATS) st[ST_MATCHES] += (dn.flags & NODE_COMPLETION) ? 1 : 0;
+        if (!(dn.flags & NODE_INNER)) return false;
+        // the child partial match (Algo 3 l.665-669)
+#pragma unroll
+        for (int k = 0; k < MAXV; k++) y.m2g[k] = m2g[k];
+        if (dn.n_new == 2) {
+            lane::m2g_set<MAXV>(y.m2g, dn.nv - 2u, e1);
+            lane::m2g_set<MAXV>(y.m2g, dn.nv - 1u, e2);
+        } else if (dn.n_new == 1) {
+            lane::m2g_set<MAXV>(y.m2g, dn.nv - 1u, e1);
+        }
+        y.node = hit;
+        y.nv = dn.nv;
+        y.tr_prev = etr;
+        y.h = h;
+        y.root = stk[5 * CAP + pi];
+        y.P = P;
+        y_lo = glob ? 0u : pos + 1;
+        y_end = glob ? 0u : p0 + stk[2 * CAP + pi];
+        y_out = out;
+        if (STATS) st[ST_NODES]++;
+        return true;
+    };
+
     for (;;) {
-        // ---- the top pieces: candidate counts and their running sum (top first)
+        // ---- the top 64 pieces: candidate counts and their running sum (top first); lane l holds
+        // pieces l and l + 32
         const uint32_t top = ps;
-        const uint32_t pn = lane_id < top ? stk[2 * CAP + top - 1 - lane_id] : 0u;
-        uint32_t incl = pn;
+        const uint32_t pn0 = lane_id < top ? stk[2 * CAP + top - 1 - lane_id] : 0u;
+        const uint32_t pn1 = lane_id + 32 < top ? stk[2 * CAP + top - 33 - lane_id] : 0u;
+        uint32_t incl0 = pn0, incl1 = pn1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(kFull, incl, o);
-            if (lane_id >= (uint32_t)o) incl += v;
+            const uint32_t v0 = __shfl_up_sync(kFull, incl0, o);
+            const uint32_t v1 = __shfl_up_sync(kFull, incl1, o);
+            if (lane_id >= (uint32_t)o) {
+                incl0 += v0;
+                incl1 += v1;
+            }
         }
-        const uint32_t tot = __shfl_sync(kFull, incl, 31);
+        const uint32_t tot0 = __shfl_sync(kFull, incl0, 31);
+        incl1 += tot0;
+        const uint32_t tot = __shfl_sync(kFull, incl1, 31);
 
-        bfs::PM<MAXV> x;   // this lane's new partial match: an item, or a child found this round
-        bool has = false;
+        bfs::PM<MAXV> x;   // this lane's new partial match: an item, or the first slot's child
+        bool has = false, has_b = false;
         uint32_t c_lo = 0, c_end = 0;  // a child's continuation window on its parent's list
         bool c_out = false;
         if (top == 0 && sp_top > 0) {
@@ -402,106 +529,58 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
             if (STATS && lane_id == 0) st[ST_ROOTS] += take;
         } else {
             if (top == 0) break;  // no items left, nothing stacked or spilled
-            // ---- this round: T entries, one per lane, from the top pieces (the last one possibly split)
-            const uint32_t T = min(tot, 32u);
-            const uint32_t excl = incl - pn;
-            const bool pc = lane_id < top && excl < T;  // this piece contributes entries
-            const uint32_t smask = __reduce_or_sync(kFull, pc ? (1u << excl) : 0u);
-            const uint32_t kf = __popc(__ballot_sync(kFull, lane_id < top && incl <= T));  // taken whole
-            const bool act = lane_id < T;
-            const uint32_t upto = smask & ((2u << lane_id) - 1u);
-            const uint32_t pi = top - 1 - (act ? (uint32_t)__popc(upto) - 1u : 0u);  // this lane's piece
-            const uint32_t at = lane_id - (31 - __clz(upto | 1u));                    // offset in the piece
-            bool valid = false;
-            if (act) {
-                const uint32_t g = stk[0 * CAP + pi];
-                const uint32_t p0 = stk[1 * CAP + pi];
-                const uint32_t pos = p0 + at;
-                const uint32_t tp = stk[3 * CAP + pi];
-                const uint32_t h = stk[4 * CAP + pi];
-                uint32_t m2g[MAXV];
-#pragma unroll
-                for (int k = 0; k < MAXV; k++) m2g[k] = stk[(6 + k) * CAP + pi];
-                const DGroup G = s_groups[g];
-                const bool glob = GEN && G.kind == ANCHOR_GLOBAL;
-                // successor pointers of the entry's edge, loaded with the entry (no extra round
-                // trip) when a child of this group locates a window from them
-                const bool needp = G.n_inner && (g >= lane::kGwMax || ((s_np[g >> 5] >> (g & 31)) & 1u));
-                uint32_t etr, e1, e2 = 0;
-                uint4 P = make_uint4(0, 0, 0, 0);
-                if (glob) {
-                    etr = __ldg(p.tr + pos);
-                    e1 = __ldg(p.src + pos);
-                    e2 = __ldg(p.dst + pos);
-                    if (needp) P = __ldg(p.eptr + pos);
-                } else {
-                    const bool out = G.kind == ANCHOR_OUT;
-                    const uint2 e = __ldg((out ? p.out_ent : p.in_ent) + pos);
-                    etr = e.x;
-                    e1 = e.y;
-                    if (needp) P = __ldg((out ? p.out_ptr : p.in_ptr) + pos);
-                    c_lo = pos + 1;
-                    c_end = p0 + stk[2 * CAP + pi];
-                    c_out = out;
-                }
-                valid = etr > tp && etr <= h;
-                uint32_t cls;
-                if (glob)
-                    cls = (e1 != e2 && lane::classify<MAXV>(m2g, e1) == CLS_NEW &&
-                           lane::classify<MAXV>(m2g, e2) == CLS_NEW) ? CLS_NEW : 0xFEu;
-                else
-                    cls = lane::classify<MAXV>(m2g, e1);
-                uint32_t hit = kNone;
-                if (G.child_end - G.child_begin <= 4 && g < lane::kGwMax) {
-                    const uint32_t eq = __vcmpeq4(s_gw[g], cls * 0x01010101u);
-                    hit = eq ? G.child_begin + ((__ffs(eq) - 1) >> 3) : kNone;
-                } else {
-                    hit = bfs::find_child(s_nodes, G, cls);
-                }
-                if (valid && hit != kNone) {
-                    const lane::LNode dn = s_nodes[hit];
-                    if (dn.flags & NODE_COMPLETION) cnt_add(dn.slot);
-                    if (STATS) st[ST_MATCHES] += (dn.flags & NODE_COMPLETION) ? 1 : 0;
-                    if (dn.flags & NODE_INNER) {  // the child partial match (Algo 3 l.665-669)
-                        has = true;
-#pragma unroll
-                        for (int k = 0; k < MAXV; k++) x.m2g[k] = m2g[k];
-                        if (dn.n_new == 2) {
-                            lane::m2g_set<MAXV>(x.m2g, dn.nv - 2u, e1);
-                            lane::m2g_set<MAXV>(x.m2g, dn.nv - 1u, e2);
-                        } else if (dn.n_new == 1) {
-                            lane::m2g_set<MAXV>(x.m2g, dn.nv - 1u, e1);
-                        }
-                        x.node = hit;
-                        x.nv = dn.nv;
-                        x.tr_prev = etr;
-                        x.h = h;
-                        x.root = stk[5 * CAP + pi];
-                        x.P = P;
-                        if (STATS) st[ST_NODES]++;
-                    }
-                }
-            }
-            if (STATS) {
-                const uint32_t nv = __popc(__ballot_sync(kFull, valid));
-                if (lane_id == 0) {
-                    st[ST_BATCHES]++;
-                    st[ST_PROBES] += T;
-                    st[ST_ENTRIES] += nv;
-                }
+            // ---- this round: T <= 64 entries, two slots per lane (lane and lane + 32), from the top
+            // pieces (the last one possibly split)
+            const uint32_t T = min(tot, 64u);
+            const uint32_t x0 = incl0 - pn0, x1 = incl1 - pn1;  // first slot of pieces lane, lane+32
+            const bool pc0 = lane_id < top && x0 < T, pc1 = lane_id + 32 < top && x1 < T;
+            const uint32_t lo_c = (pc0 && x0 < 32 ? 1u << x0 : 0u) | (pc1 && x1 < 32 ? 1u << x1 : 0u);
+            const uint32_t hi_c = (pc0 && x0 >= 32 ? 1u << (x0 - 32) : 0u) | (pc1 && x1 >= 32 ? 1u << (x1 - 32) : 0u);
+            const uint32_t mlo = __reduce_or_sync(kFull, lo_c), mhi = __reduce_or_sync(kFull, hi_c);
+            if (pc0) own[x0] = lane_id;
+            if (pc1) own[x1] = lane_id + 32;
+            __syncwarp();
+            const uint32_t kf = __popc(__ballot_sync(kFull, lane_id < top && incl0 <= T)) +
+                                __popc(__ballot_sync(kFull, lane_id + 32 < top && incl1 <= T));  // taken whole
+            const unsigned le = (2u << lane_id) - 1u;
+            const uint32_t sa = 31 - __clz((mlo & le) | 1u);  // first slot of slot lane's piece
+            const uint32_t hb = mhi & le;
+            const uint32_t sb = hb ? 63 - __clz(hb) : 31 - __clz(mlo | 1u);
+            const bool act_a = lane_id < T, act_b = lane_id + 32 < T;
+            uint32_t b_lo = 0, b_end = 0;
+            bool b_out = false;
+            bfs::PM<MAXV> yb;
+            if (act_a) has = test_slot(top - 1 - own[sa], lane_id - sa, x, c_lo, c_end, c_out);
+            if (act_b) has_b = test_slot(top - 1 - own[sb], lane_id + 32 - sb, yb, b_lo, b_end, b_out);
+            if (has_b) stage_put<MAXV>(sgb, lane_id, yb, b_lo, b_end, b_out);
+            if (STATS && lane_id == 0) {
+                st[ST_BATCHES]++;
+                st[ST_PROBES] += T;
             }
             __syncwarp();
-            // ---- pop the pieces taken whole; advance the split one
-            if (lane_id == kf && kf < top && excl < T) {
-                stk[1 * CAP + top - 1 - kf] += T - excl;
-                stk[2 * CAP + top - 1 - kf] -= T - excl;
+            // ---- pop the pieces taken whole; advance the split one (piece kf)
+            if (kf < top) {
+                const uint32_t xk = kf < 32 ? x0 : x1;
+                if ((kf & 31) == lane_id && xk < T) {
+                    stk[1 * CAP + top - 1 - kf] += T - xk;
+                    stk[2 * CAP + top - 1 - kf] -= T - xk;
+                }
             }
             ps = top - kf;
             __syncwarp();
         }
-        // ---- the new partial matches' windows go on top of the stack (depth first)
-        if (__any_sync(kFull, has))
-            open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, has, x, c_lo, c_end, c_out, my_cnt, s_tot, st);
+        // ---- the new partial matches' windows go on top of the stack (depth first): the first
+        // slot's children (or the items) from registers, then the second slot's from staging
+        for (int half = 0; half < 2; half++) {
+            if (half == 1) {
+                if (!__any_sync(kFull, has_b)) break;
+                has = has_b;
+                if (has_b) stage_get<MAXV>(sgb, lane_id, x, c_lo, c_end, c_out, s_nodes);
+            }
+            if (__any_sync(kFull, has))
+                open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, has, x, c_lo, c_end, c_out,
+                                                 my_cnt, s_tot, st);
+        }
     }
 
     // ---- counters: lanes -> block -> global, once per block

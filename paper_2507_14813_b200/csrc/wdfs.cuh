@@ -73,29 +73,30 @@ __host__ __device__ inline size_t smem_bytes(uint32_t nn, uint32_t ng, uint32_t 
 }
 
 // Length of a window: entries [lo, lo + n) are the entries of list `ent` from lo with time
-// rank <= h, stopping at the list's sentinel (index `sent`).  Six independent probes at offsets
-// 0, 1, 3, 7, 15, 31 bracket n (lists are padded past their last sentinel, so lo + 31 is in
-// bounds; an index at or past the sentinel is out whatever it holds); a bisection inside the
-// bracket makes it exact (<= 4 dependent loads on lines the probes just brought in).  Windows of
-// >= 32 entries gallop first (rare).
+// rank <= h, stopping at the list's sentinel (index `sent`).  Four independent probes at offsets
+// 0, 1, 3, 7 (two 32-byte sectors; lists are padded past their last sentinel, so lo + 7 is in
+// bounds; an index at or past the sentinel is out whatever it holds) bracket n; a bisection inside
+// the bracket makes it exact (<= 2 dependent loads on the sectors the probes just brought in).
+// Windows of >= 8 entries gallop on (15, 31, 63, ...: dependent loads, the rarer case).  Wider
+// unconditional probes cost more L2 sectors than they save round trips (profiles/README.md r2).
 __device__ __forceinline__ bool in_window(const uint2 *ent, uint32_t lo, uint32_t o, uint32_t sent, uint32_t h) {
     return lo + o < sent && __ldg(&ent[lo + o].x) <= h;
 }
 __device__ __forceinline__ uint32_t window_len(const uint2 *ent, uint32_t lo, uint32_t sent, uint32_t h) {
-    const uint32_t o[6] = {0, 1, 3, 7, 15, 31};
-    uint32_t v[6];
+    const uint32_t o[4] = {0, 1, 3, 7};
+    uint32_t v[4];
 #pragma unroll
-    for (int k = 0; k < 6; k++) v[k] = __ldg(&ent[lo + o[k]].x);
+    for (int k = 0; k < 4; k++) v[k] = __ldg(&ent[lo + o[k]].x);
     uint32_t b = kNone, a = 0;  // out at offset b; in at every probe below it
 #pragma unroll
-    for (int k = 5; k >= 0; k--)
+    for (int k = 3; k >= 0; k--)
         if (lo + o[k] >= sent || v[k] > h) b = o[k];
     if (b == 0) return 0;
     if (b != kNone) {
         a = b == 1 ? 0 : (b - 1) / 2;  // the previous probe offset (in)
-    } else {  // >= 32 entries: gallop
-        a = 31;
-        b = 63;
+    } else {  // >= 8 entries: gallop
+        a = 7;
+        b = 15;
         for (;;) {
             if (lo + b >= sent) {
                 b = sent - lo;

@@ -9,7 +9,8 @@ if [ -n "$1" ]; then
 fi
 for F in $FORMS; do
   K=${F%%+*}; X=${F#*+}; [ "$X" == "$F" ] && X=""
+  N=$(echo "$F" | tr '/=+' '___')
   env MAYURA_KERNEL=$K $X timeout 900 python bench.py --config $C --profile --steps 10 --warmup 3 \
-    > gpurun_out/ab_${TAG}_${C}_${F}.json 2> gpurun_out/ab_${TAG}_${C}_${F}.err
-  echo "$C $F rc=$? $(python -c "import json,sys; d=json.load(open('gpurun_out/ab_${TAG}_${C}_${F}.json')); print('ms %.3f kern %.3f form %s counts %s' % (d['ms_per_step'], d['roofline']['kernel_ms'], d['roofline']['kernel_form'], sum(d['counts'].values())))" 2>&1 | tail -1)"
+    > gpurun_out/ab_${TAG}_${C}_${N}.json 2> gpurun_out/ab_${TAG}_${C}_${N}.err
+  echo "$C $F rc=$? $(python -c "import json,sys; d=json.load(open('gpurun_out/ab_${TAG}_${C}_${N}.json')); print('ms %.3f kern %.3f form %s counts %s' % (d['ms_per_step'], d['roofline']['kernel_ms'], d['roofline']['kernel_form'], sum(d['counts'].values())))" 2>&1 | tail -1)"
 done

@@ -382,6 +382,10 @@ mayura_status launch_wdfs(mayura_graph_s *g, wdfs::WParams w, uint32_t max_verti
         g->fresh_alloc = false;
     }
     w.spill = g->d_wspill;
+    {  // MAYURA_WDFS_CHUNK: items per cursor grab (tuning; default 256)
+        const char *ev = getenv("MAYURA_WDFS_CHUNK");
+        w.chunk_max = ev ? std::max<uint32_t>(32u, (uint32_t)atoi(ev) & ~31u) : 256u;
+    }
     cudaError_t e;
     if (max_vertices <= 4) e = launch_wdfs_v<4>(w, generic, stats, s, sms);
     else if (max_vertices <= 6) e = launch_wdfs_v<6>(w, generic, stats, s, sms);

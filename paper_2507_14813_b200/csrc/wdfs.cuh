@@ -59,6 +59,7 @@ struct WParams {
     uint32_t direct;         // 1: the items are the root edges [r0, r0 + n_roots) themselves
     uint32_t o_cnt, o_stk;   // dynamic shared memory offsets: lane counters, stacks
     uint32_t lanecnt;        // 1: per-lane u32 counters; 0: block u64 atomics (many slots)
+    uint32_t chunk_max;      // items a warp takes from the cursor at once (multiple of 32)
 };
 
 __host__ __device__ inline size_t off_cnt(uint32_t nn, uint32_t ng, uint32_t ns) {
@@ -497,7 +498,7 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
                 if (lane_id == 0) {
                     const uint32_t cur = *(volatile uint32_t *)w.lb;
                     const uint32_t rem = cur < n_items ? n_items - cur : 0u;
-                    sz = max(32u, min(256u, (rem / (4u * gridDim.x * kWarps)) & ~31u));
+                    sz = max(32u, min(w.chunk_max, (rem / (4u * gridDim.x * kWarps)) & ~31u));
                     b = atomicAdd(w.lb, sz);
                 }
                 b = __shfl_sync(kFull, b, 0);

@@ -384,7 +384,7 @@ mayura_status launch_wdfs(mayura_graph_s *g, wdfs::WParams w, uint32_t max_verti
     w.spill = g->d_wspill;
     {  // MAYURA_WDFS_CHUNK: items per cursor grab (tuning; default 256)
         const char *ev = getenv("MAYURA_WDFS_CHUNK");
-        w.chunk_max = ev ? std::max<uint32_t>(32u, (uint32_t)atoi(ev) & ~31u) : 256u;
+        w.chunk_max = ev ? std::max<uint32_t>(32u, (uint32_t)atoi(ev) & ~31u) : 32u;  // r2 sweep: 32 best
     }
     cudaError_t e;
     if (max_vertices <= 4) e = launch_wdfs_v<4>(w, generic, stats, s, sms);

@@ -37,7 +37,10 @@ namespace wdfs {
 
 constexpr int kWB = 128;                 // threads per block
 constexpr int kWarps = kWB / 32;
-constexpr int kCap = 128;                // pieces per warp stack in shared memory
+#ifndef WDFS_CAP
+#define WDFS_CAP 128
+#endif
+constexpr int kCap = WDFS_CAP;           // pieces per warp stack in shared memory
 constexpr int kCapSmall = 64;            // test instance (MAYURA_WDFS_SMALL=1): spills early and often
 constexpr uint8_t NODE_NEEDP = 16;       // LNode flag: a group of the node needs its edge's successor
                                          // pointers (a START_P* group that is not a same-list continuation)

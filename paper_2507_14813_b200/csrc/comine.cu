@@ -417,9 +417,10 @@ cudaError_t launch_lane(const lane::LParams &p, uint32_t max_vertices, bool stat
 }
 
 // Kernel form (MAYURA_KERNEL overrides): "mixed" (heavy roots in the flat form, light roots
-// depth-first), "flat" (level-synchronous, entry-parallel; flat.cuh),
-// "hybrid" (one breadth-first level + the depth-first lane kernel), "lane", "bfs".  Default:
-// flat when the graph arrays fit in L2, else hybrid.  Measured (profiles/README.md r04): flat
+// depth-first), "flat" (level-synchronous, entry-parallel; flat.cuh), "warp" (the warp-
+// synchronous depth-first kernel straight from the roots; wdfs.cuh), "hybrid" (one breadth-first
+// level + the warp kernel, MAYURA_DFS=lane: + the lane kernel), "lane", "bfs".  Default: flat when
+// the graph arrays fit in L2, else warp (r2: C4 92.7 ms hybrid-lane -> 75.4 ms warp).  Measured (profiles/README.md r04): flat
 // C1 0.172 -> 0.076 ms, C2 0.527 -> 0.321 ms; on DRAM-resident graphs its per-level frontier
 // and window-piece traffic loses (C3 4.9 ms hybrid vs 7.8 ms flat).
 enum KernelKind { K_HYBRID = 0, K_LANE = 1, K_BFS = 2, K_FLAT = 3, K_MIXED = 4, K_WARP = 5 };
@@ -436,7 +437,7 @@ KernelKind kernel_kind(const mayura_graph_s *g) {  // read per call (tests switc
     if (e && std::strcmp(e, "hybrid") == 0) return K_HYBRID;
     if (e && std::strcmp(e, "mixed") == 0) return K_MIXED;
     if (e && std::strcmp(e, "warp") == 0) return K_WARP;
-    return l2_resident(g) ? K_FLAT : K_HYBRID;
+    return l2_resident(g) ? K_FLAT : K_WARP;
 }
 // hybrid: a root is split breadth-first only if one of its root-node windows has >= this
 // many entries; the breadth-first level lists the light ones for the depth-first kernel.
@@ -962,7 +963,9 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
         for (size_t i = 1; i < tabs.size(); i++) mv = std::max(mv, tabs[i].max_vertices);
         const KernelKind kind = kernel_kind(g);
         if (kind != K_LANE && n_roots > 0) {
-            const uint32_t lv = kind == K_BFS || kind == K_FLAT || kind == K_MIXED ? 2u : std::min(hybrid_levels(), 2u);
+            // the warp form needs no frontier buffers (its stacks live in shared memory + the spill area)
+            const uint32_t lv = kind == K_BFS || kind == K_FLAT || kind == K_MIXED ? 2u
+                                : kind == K_HYBRID ? std::min(hybrid_levels(), 2u) : 0u;
             if (lv > 0) st = ensure_bfs_buffers(g, rec_words(mv), lv >= 2 ? 2 : 1);
             if (st != MAYURA_OK) return st;
             if (kind == K_FLAT || kind == K_MIXED) st = ensure_flat_win(g);
@@ -1329,7 +1332,7 @@ void stash_scratch(mayura_graph_s *g) {
     if (g->device < 0 || g->device >= 64) return;
     std::lock_guard<std::mutex> lk(g_scratch_mu);
     ScratchSet &c = g_scratch[g->device];
-    if (!g->d_bfs_ctl || !g->d_light || !g->d_queue) return;  // nothing reusable (freed with the graph)
+    if (!g->d_queue) return;  // nothing reusable (freed with the graph); other members may be null
     if (c.valid) free_scratch_set(c);
     c.valid = true;
     c.e_cap = g->E;

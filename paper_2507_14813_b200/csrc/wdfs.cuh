@@ -38,7 +38,7 @@ namespace wdfs {
 constexpr int kWB = 128;                 // threads per block
 constexpr int kWarps = kWB / 32;
 #ifndef WDFS_CAP
-#define WDFS_CAP 128
+#define WDFS_CAP 96  // r2 sweep on C4: 64 / 80 / 96 / 128 -> 78.1 / 77.3 / 75.4 / 77.8 ms
 #endif
 constexpr int kCap = WDFS_CAP;           // pieces per warp stack in shared memory
 constexpr int kCapSmall = 64;            // test instance (MAYURA_WDFS_SMALL=1): spills early and often

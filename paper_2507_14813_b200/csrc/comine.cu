@@ -382,6 +382,7 @@ mayura_status launch_wdfs(mayura_graph_s *g, wdfs::WParams w, uint32_t max_verti
         g->fresh_alloc = false;
     }
     w.spill = g->d_wspill;
+    w.ent_len = (uint32_t)(g->E + g->V);
     {  // MAYURA_WDFS_CHUNK: items per cursor grab (tuning; default 256)
         const char *ev = getenv("MAYURA_WDFS_CHUNK");
         w.chunk_max = ev ? std::max<uint32_t>(32u, (uint32_t)atoi(ev) & ~31u) : 32u;  // r2 sweep: 32 best

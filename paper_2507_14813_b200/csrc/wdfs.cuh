@@ -45,6 +45,22 @@ constexpr int kCapSmall = 64;            // test instance (MAYURA_WDFS_SMALL=1):
 constexpr uint8_t NODE_NEEDP = 16;       // LNode flag: a group of the node needs its edge's successor
                                          // pointers (a START_P* group that is not a same-list continuation)
 
+// WDFS_CHECK builds (A/B variant, tools/gpu_dbg.sh): device-side bounds checks that print and trap
+#ifdef WDFS_CHECK
+#define WCHECK(cond, fmt, ...)                                                                      \
+    do {                                                                                            \
+        if (!(cond)) {                                                                              \
+            printf("WDFS_CHECK %s:%d block %d lane %d: " fmt "\n", __FILE__, __LINE__, blockIdx.x,   \
+                   threadIdx.x, __VA_ARGS__);                                                       \
+            __trap();                                                                               \
+        }                                                                                           \
+    } while (0)
+#else
+#define WCHECK(cond, fmt, ...) \
+    do {                       \
+    } while (0)
+#endif
+
 template <int MAXV>
 struct Piece {
     // words per piece: 0 group, 1 pos, 2 n, 3 tr_prev, 4 h, 5 root, 6.. m2g[MAXV]
@@ -63,6 +79,7 @@ struct WParams {
     uint32_t o_cnt, o_stk;   // dynamic shared memory offsets: lane counters, stacks
     uint32_t lanecnt;        // 1: per-lane u32 counters; 0: block u64 atomics (many slots)
     uint32_t chunk_max;      // items a warp takes from the cursor at once (multiple of 32)
+    uint32_t ent_len;        // adjacency entries (E + V, sentinels included) -- WDFS_CHECK only
 };
 
 __host__ __device__ inline size_t off_cnt(uint32_t nn, uint32_t ng, uint32_t ns) {
@@ -155,6 +172,8 @@ __device__ __forceinline__ uint32_t window(const bfs::BParams &p, const DGroup &
         lo = a;
     }
     n = window_len(ent, lo, sent, x.h);
+    WCHECK(lo <= sent && lo + n <= sent, "window lo %u n %u sent %u start %u anchor %u v %u", lo, n, sent,
+           (unsigned)G.start, (unsigned)G.anchor, v);
     return lo;
 }
 
@@ -265,6 +284,7 @@ __device__ __forceinline__ void open_push(const WParams &w, const lane::LNode *s
             if ((same >> q) & 1u) {
                 lo = c_lo;
                 n = c_end > c_lo ? c_end - c_lo : 0u;
+                WCHECK(c_lo <= c_end + 1, "continuation c_lo %u c_end %u node %u", c_lo, c_end, x.node);
             } else {
                 lo = window<MAXV, GEN>(p, s_groups[gb + q], x, n);
             }
@@ -395,6 +415,10 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
         const uint32_t g = stk[0 * CAP + pi];
         const uint32_t p0 = stk[1 * CAP + pi];
         const uint32_t pos = p0 + at;
+        WCHECK(pi < ps && at < stk[2 * CAP + pi] && g < p.n_groups, "slot pi %u ps %u at %u n %u g %u", pi, ps, at,
+               stk[2 * CAP + pi], g);
+        WCHECK((s_groups[g].kind == ANCHOR_GLOBAL && pos < p.E) || (s_groups[g].kind != ANCHOR_GLOBAL && pos < w.ent_len),
+               "entry pos %u (p0 %u at %u) kind %u", pos, p0, at, (unsigned)s_groups[g].kind);
         const uint32_t tp = stk[3 * CAP + pi];
         const uint32_t h = stk[4 * CAP + pi];
         const DGroup G = s_groups[g];

@@ -53,6 +53,9 @@ def _load():
         lib.oracle_bruteforce.restype = i32
         lib.oracle_backtrack.argtypes = [P, P, P, u64, u32, P, P, u32, i64, u64, u64, i32, P]
         lib.oracle_backtrack.restype = i32
+        lib.oracle_backtrack_ranges.argtypes = [P, P, P, u64, u32, P, P, u32, i64, P, u32, i32, P, P,
+                                                ctypes.c_double, P]
+        lib.oracle_backtrack_ranges.restype = i32
         lib.oracle_enumerate.argtypes = [P, P, P, u64, u32, P, u32, i64, u64, u64, P, u64, P]
         lib.oracle_enumerate.restype = i32
         lib.oracle_sorted_order.argtypes = [P, u64, P]
@@ -106,6 +109,32 @@ def backtrack(src, dst, t, n_vertices: int, motifs: Sequence[Sequence[Tuple[int,
     if rc != 0:
         raise OracleError("oracle_backtrack failed rc=%d" % rc)
     return [int(x) for x in out]
+
+
+def backtrack_ranges(src, dst, t, n_vertices: int, motifs: Sequence[Sequence[Tuple[int, int]]],
+                     delta: int, ranges: Sequence[Tuple[int, int]], threads: Optional[int] = None,
+                     budget_s: float = 0.0):
+    """O2 over several root ranges of one graph build: ([[count per motif] per mined range],
+    build seconds, mining seconds).  budget_s > 0: ranges are started only while less than
+    budget_s seconds of mining have elapsed, so the result covers a prefix of `ranges`."""
+    lib = _load()
+    s, d, tt = _arr(src, np.uint32), _arr(dst, np.uint32), _arr(t, np.int64)
+    E = s.size
+    me = _arr([x for m in motifs for e in m for x in e], np.uint32)
+    ml = _arr([len(m) for m in motifs], np.uint32)
+    rg = _arr([x for r in ranges for x in r], np.uint64)
+    out = np.zeros(len(ranges) * len(motifs), np.uint64)
+    secs = np.zeros(2, np.float64)
+    done = np.zeros(1, np.uint32)
+    nt = threads if threads is not None else (os.cpu_count() or 1)
+    rc = lib.oracle_backtrack_ranges(_ptr(s), _ptr(d), _ptr(tt), E, n_vertices, _ptr(me), _ptr(ml),
+                                     len(motifs), int(delta), _ptr(rg), len(ranges), nt, _ptr(out), _ptr(secs),
+                                     float(budget_s), _ptr(done))
+    if rc != 0:
+        raise OracleError("oracle_backtrack_ranges failed rc=%d" % rc)
+    k = len(motifs)
+    return ([[int(x) for x in out[i * k:(i + 1) * k]] for i in range(int(done[0]))],
+            float(secs[0]), float(secs[1]))
 
 
 def enumerate_matches(src, dst, t, n_vertices: int, motif: Sequence[Tuple[int, int]], delta: int,

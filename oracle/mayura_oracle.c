@@ -308,14 +308,29 @@ static void *o2_thread(void *arg) {
     return NULL;
 }
 
-/* Mine each of n_motifs motifs independently over roots [root_begin, root_end).
+#include <time.h>
+static double o2_now(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+/* Mine each of n_motifs motifs independently over each of n_ranges root ranges
+ * [ranges[2r], ranges[2r+1]) of ONE graph build (the build -- sort + adjacency -- costs tens of
+ * seconds at 63 M edges, so sampled runs query many ranges of one build).
  * motif_edges: concatenated (u,v) pairs; motif_len: edges per motif.
- * counts_out[i] receives the count of motif i.  n_threads <= 0: 1 thread. */
-int oracle_backtrack(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t E,
-                     uint32_t V, const uint32_t *motif_edges, const uint32_t *motif_len,
-                     uint32_t n_motifs, int64_t delta, uint64_t root_begin, uint64_t root_end,
-                     int n_threads, uint64_t *counts_out) {
-    if (n_motifs == 0 || delta < 0 || root_begin > root_end || root_end > E) return -1;
+ * counts_out[r * n_motifs + i] receives the count of motif i over range r.
+ * secs_out (may be NULL): [0] graph build seconds, [1] mining seconds.  n_threads <= 0: 1.
+ * budget_s > 0: no range is started once budget_s seconds of mining have elapsed (at least one
+ * range runs); *n_done (may be NULL) receives the number of ranges mined (a prefix). */
+int oracle_backtrack_ranges(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t E,
+                            uint32_t V, const uint32_t *motif_edges, const uint32_t *motif_len,
+                            uint32_t n_motifs, int64_t delta, const uint64_t *ranges, uint32_t n_ranges,
+                            int n_threads, uint64_t *counts_out, double *secs_out, double budget_s,
+                            uint32_t *n_done) {
+    if (n_motifs == 0 || delta < 0) return -1;
+    for (uint32_t r = 0; r < n_ranges; r++)
+        if (ranges[2 * r] > ranges[2 * r + 1] || ranges[2 * r + 1] > E) return -1;
     uint64_t off = 0;
     for (uint32_t i = 0; i < n_motifs; i++) {
         if (motif_len[i] == 0 || motif_len[i] > OR_MAX_EDGES) return -1;
@@ -325,39 +340,58 @@ int oracle_backtrack(const uint32_t *src, const uint32_t *dst, const int64_t *t,
         }
         off += motif_len[i];
     }
+    double t0 = o2_now();
     og_graph g;
     int rc = og_build(&g, src, dst, t, E, V);
     if (rc) return rc;
+    double t1 = o2_now();
     if (n_threads < 1) n_threads = 1;
     pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * n_threads);
     o2_worker *wk = (o2_worker *)calloc(n_threads, sizeof(o2_worker));
     if (!th || !wk) { free(th); free(wk); og_free(&g); return -3; }
-    off = 0;
-    for (uint32_t i = 0; i < n_motifs; i++) {
-        uint32_t mu[OR_MAX_EDGES], mv[OR_MAX_EDGES];
-        for (uint32_t j = 0; j < motif_len[i]; j++) {
-            mu[j] = motif_edges[2 * (off + j)]; mv[j] = motif_edges[2 * (off + j) + 1];
+    uint32_t r = 0;
+    for (; r < n_ranges; r++) {
+        if (budget_s > 0 && r > 0 && o2_now() - t1 >= budget_s) break;  /* time-bounded sample */
+        off = 0;
+        for (uint32_t i = 0; i < n_motifs; i++) {
+            uint32_t mu[OR_MAX_EDGES], mv[OR_MAX_EDGES];
+            for (uint32_t j = 0; j < motif_len[i]; j++) {
+                mu[j] = motif_edges[2 * (off + j)]; mv[j] = motif_edges[2 * (off + j) + 1];
+            }
+            off += motif_len[i];
+            o2_shared sh;
+            sh.g = &g; sh.mu = mu; sh.mv = mv; sh.m = motif_len[i]; sh.delta = delta;
+            sh.next = ranges[2 * r]; sh.end = ranges[2 * r + 1]; sh.chunk = 256;
+            pthread_mutex_init(&sh.lock, NULL);
+            for (int w = 0; w < n_threads; w++) {
+                wk[w].sh = &sh; wk[w].count = 0; wk[w].err = 0;
+                pthread_create(&th[w], NULL, o2_thread, &wk[w]);
+            }
+            uint64_t total = 0;
+            for (int w = 0; w < n_threads; w++) {
+                pthread_join(th[w], NULL);
+                total += wk[w].count;
+                if (wk[w].err) rc = wk[w].err;
+            }
+            pthread_mutex_destroy(&sh.lock);
+            counts_out[(uint64_t)r * n_motifs + i] = total;
         }
-        off += motif_len[i];
-        o2_shared sh;
-        sh.g = &g; sh.mu = mu; sh.mv = mv; sh.m = motif_len[i]; sh.delta = delta;
-        sh.next = root_begin; sh.end = root_end; sh.chunk = 256;
-        pthread_mutex_init(&sh.lock, NULL);
-        for (int w = 0; w < n_threads; w++) {
-            wk[w].sh = &sh; wk[w].count = 0; wk[w].err = 0;
-            pthread_create(&th[w], NULL, o2_thread, &wk[w]);
-        }
-        uint64_t total = 0;
-        for (int w = 0; w < n_threads; w++) {
-            pthread_join(th[w], NULL);
-            total += wk[w].count;
-            if (wk[w].err) rc = wk[w].err;
-        }
-        pthread_mutex_destroy(&sh.lock);
-        counts_out[i] = total;
     }
+    if (secs_out) { secs_out[0] = t1 - t0; secs_out[1] = o2_now() - t1; }
+    if (n_done) *n_done = r;
     free(th); free(wk); og_free(&g);
     return rc;
+}
+
+/* Mine each of n_motifs motifs independently over roots [root_begin, root_end) (one range of
+ * oracle_backtrack_ranges).  counts_out[i] receives the count of motif i. */
+int oracle_backtrack(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t E,
+                     uint32_t V, const uint32_t *motif_edges, const uint32_t *motif_len,
+                     uint32_t n_motifs, int64_t delta, uint64_t root_begin, uint64_t root_end,
+                     int n_threads, uint64_t *counts_out) {
+    const uint64_t rg[2] = {root_begin, root_end};
+    return oracle_backtrack_ranges(src, dst, t, E, V, motif_edges, motif_len, n_motifs, delta, rg, 1,
+                                   n_threads, counts_out, NULL, 0.0, NULL);
 }
 
 /* Exposes the oracle's own (t, input rank) sort, so tests can check that the

@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
             }
             __syncwarp();
             // ---- pop the pieces taken whole; advance the split one (piece kf)
-            if (kf < top) {
+            if (kf < top && kf < 64) {  // (kf = 64: the 64 examined pieces were all taken whole)
                 const uint32_t xk = kf < 32 ? x0 : x1;
                 if ((kf & 31) == lane_id && xk < T) {
                     stk[1 * CAP + top - 1 - kf] += T - xk;

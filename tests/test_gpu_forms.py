@@ -138,3 +138,12 @@ def test_form_small_warp_stacks(M, oracle_mod, monkeypatch, hook):
         src, dst, t, V = synth.random_graph(90 + seed, 6, 6000, 3000, 0.01)
         motifs = synth.group(synth.GROUP_C4)
         assert run(M, src, dst, t, V, motifs, 40) == oracle_mod.backtrack(src, dst, t, V, motifs, 40)
+
+
+def test_form_many_single_entry_windows(M, oracle_mod):
+    """Sparse graphs whose windows mostly hold one entry: the warp kernel's rounds then take 64
+    one-entry pieces whole (the case where no piece is split), and hub-free roots dominate."""
+    for seed in range(3):
+        src, dst, t, V = synth.random_graph(400 + seed, 3000, 60_000, 200_000, 0.002)
+        motifs = synth.group(synth.GROUP_C2) + [synth.MOTIFS["recip2"], synth.MOTIFS["path2"]]
+        assert run(M, src, dst, t, V, motifs, 400) == oracle_mod.backtrack(src, dst, t, V, motifs, 400)

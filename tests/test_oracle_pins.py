@@ -284,3 +284,13 @@ def test_time_translation_invariance(oracle_mod):
             ts = t + np.int64(shift)
             assert oracle_mod.backtrack(src, dst, ts, V, motifs, delta) == base, (seed, shift)
         assert [oracle_mod.bruteforce(src, dst, t - np.int64(1 << 62), V, mo, delta) for mo in motifs[:4]] == base[:4]
+
+
+def test_backtrack_ranges_equals_single_ranges(oracle_mod):
+    """oracle_backtrack_ranges (one graph build, many root ranges) == oracle_backtrack per range."""
+    src, dst, t, V = synth.random_graph(777, 15, 400, 150)
+    motifs = synth.group(synth.GROUP_C2)
+    ranges = [(0, 37), (37, 37), (100, 180), (350, 400)]
+    per, build_s, mine_s = oracle_mod.backtrack_ranges(src, dst, t, V, motifs, 20, ranges, threads=3)
+    assert per == [oracle_mod.backtrack(src, dst, t, V, motifs, 20, root_range=r) for r in ranges]
+    assert build_s >= 0 and mine_s >= 0

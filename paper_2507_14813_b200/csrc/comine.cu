@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_scan.cuh>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX ranges (visible under nsys / ncu --nvtx)
 
 #include <algorithm>
 #include <cstdio>
@@ -29,6 +30,12 @@
 namespace mayura {
 
 namespace {
+
+// NVTX range for the scope of one C-ABI call (a no-op unless a profiler is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr uint32_t kNone = 0xffffffffu;
@@ -50,9 +57,14 @@ __device__ __forceinline__ void pdl_begin() {
 // short) then binary search
 __device__ __forceinline__ uint32_t window_end_of(const int64_t *__restrict__ T, uint32_t E, int64_t delta, uint32_t r) {
     const int64_t x = __ldg(T + r);
-    const int64_t lim = (x > INT64_MAX - delta) ? INT64_MAX : x + delta;  // delta >= 0: no overflow
+    int64_t lim = (x > INT64_MAX - delta) ? INT64_MAX : x + delta;  // delta >= 0: no overflow
     uint32_t a = r + 1, step = 1;  // invariant: T[a-1] <= lim
     uint32_t b = E;
+#ifdef MAYURA_PLANT_BUG
+    // PLANTED BUG (test build only, tests/test_planted_bug.py): the window closes BEFORE t_r + delta
+    // (t_m - t_1 < delta instead of <= delta) -- the parity suite must turn red
+    if (lim != INT64_MIN) lim -= 1;
+#endif
     while (a < E) {
         const uint32_t probe = min(E - 1, a + step - 1);
         if (__ldg(T + probe) > lim) {
@@ -1430,6 +1442,7 @@ extern "C" mayura_status mayura_load_graph(const uint32_t *src, const uint32_t *
     }
     g->device = device;
     {
+        NvtxRange nr("mayura_load_graph");
         DeviceGuard guard(device);
         drop_small_scratch(device, n_edges);
         s = build_graph_device(src, dst, t, n_edges, n_vertices, g);  // step a0 on the GPU (graph_gpu.cu)
@@ -1453,6 +1466,7 @@ extern "C" void mayura_free_graph(mayura_graph g) {
 extern "C" mayura_status mayura_comine(mayura_graph g, mayura_mgtree m, uint64_t root_begin, uint64_t root_end,
                                        void *cuda_stream, uint64_t *counts_out, int counts_on_device) {
     clear_error();
+    NvtxRange nr("mayura_comine");
     return run(g, m, root_begin, root_end, cuda_stream, counts_out, counts_on_device, 0, nullptr);
 }
 
@@ -1460,6 +1474,7 @@ extern "C" mayura_status mayura_mine_independent(mayura_graph g, mayura_mgtree m
                                                  uint64_t root_end, void *cuda_stream, uint64_t *counts_out,
                                                  int counts_on_device) {
     clear_error();
+    NvtxRange nr("mayura_mine_independent");
     return run(g, m, root_begin, root_end, cuda_stream, counts_out, counts_on_device, 1, nullptr);
 }
 
@@ -1467,6 +1482,7 @@ extern "C" mayura_status mayura_comine_ex(mayura_graph g, mayura_mgtree m, uint6
                                           void *cuda_stream, uint64_t *counts_out, int counts_on_device,
                                           int independent, void *mid_event) {
     clear_error();
+    NvtxRange nr(independent ? "mayura_comine_ex(independent)" : "mayura_comine_ex");
     return run(g, m, root_begin, root_end, cuda_stream, counts_out, counts_on_device, independent ? 1 : 0,
                nullptr, mid_event);
 }
@@ -1483,6 +1499,7 @@ extern "C" mayura_status mayura_enumerate(mayura_graph g, mayura_mgtree m, uint6
                                           void *cuda_stream, uint32_t *tuples_out, uint64_t capacity_words,
                                           int tuples_on_device, uint64_t *counts_out, uint64_t *words_needed) {
     clear_error();
+    NvtxRange nr("mayura_enumerate");
     return run_enum(g, m, root_begin, root_end, cuda_stream, tuples_out, capacity_words, tuples_on_device,
                     counts_out, words_needed);
 }

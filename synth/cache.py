@@ -55,7 +55,7 @@ def _load(hdr_path, arr_paths):
         a = np.load(arr_paths[f], mmap_mode="r")
         if list(a.shape) != hdr["shape"][f] or str(a.dtype) != hdr["dtype"][f]:
             return None
-        out.append(np.ascontiguousarray(a))
+        out.append(np.array(a))  # a writable in-memory copy (torch.from_numpy needs writable arrays)
     return out[0], out[1], out[2], int(hdr["n_vertices"])
 
 

@@ -252,11 +252,38 @@ def test_gpu_graph_build_errors(M):
         M.Graph([0, 1], [1, 7], [0, 1], 3, device=0)     # vertex id >= n_vertices
 
 
+def _heaviest_roots(src, dst, t, delta, k, hubs=64):
+    """The k roots with the most edges inside their root-node windows: out(src) and in(dst)
+    entries with t_r < t <= t_r + delta (the hub bursts of the workload; the partition proxy of
+    mayura_partition_roots grows with the same window sizes), searched among the roots incident
+    to the `hubs` highest-degree vertices.  Vectorised with (vertex, t) keys."""
+    import numpy as np
+    deg = np.bincount(src, minlength=int(max(src.max(), dst.max())) + 1) + \
+        np.bincount(dst, minlength=int(max(src.max(), dst.max())) + 1)
+    hub = np.zeros(deg.size, bool)
+    hub[np.argsort(-deg, kind="stable")[:hubs]] = True
+    cand = np.nonzero(hub[src] | hub[dst])[0]
+    tt = t - t.min()
+    span = int(tt.max()) + int(delta) + 2
+    def window_sizes(v):
+        keys = np.sort(v.astype(np.int64) * span + tt)
+        q = v[cand].astype(np.int64) * span + tt[cand]
+        return np.searchsorted(keys, q + delta, side="right") - np.searchsorted(keys, q, side="right")
+    w = window_sizes(src) + window_sizes(dst)
+    top = cand[np.argsort(-w, kind="stable")[:k]]
+    order = np.argsort(t, kind="stable")   # edge id = position in the stable time order (R1)
+    rank_t = np.empty_like(order)
+    rank_t[order] = np.arange(t.size)
+    return sorted(int(rank_t[i]) for i in top), sorted((int(x) for x in np.sort(w)[::-1][:k]), reverse=True)
+
+
 @pytest.mark.slow
 def test_config_c4_sampled_parity(M, oracle_mod):
     """C4 (63.5 M edges, delta = 1 day, 16 motifs up to 5 edges): the whole graph is mined on
-    the GPU; exact parity on sampled root ranges (the oracle cannot finish C4 in full,
-    SURVEY.md §8(d)); co-mined == independent on a sample; range additivity at full size."""
+    the GPU; exact parity per motif on 32 evenly spaced 64-root chunks and on the 8 roots with
+    the largest root-node windows (hub bursts), all from one oracle graph build (the oracle
+    cannot finish C4 in full); co-mined == independent on a sample; range
+    additivity at full size; the default (warp) form and the hybrid form agree."""
     cfg = synth.CONFIGS["C4"]
     src, dst, t, V = cfg.graph()
     g = M.Graph(src, dst, t, V, device=0)
@@ -264,14 +291,46 @@ def test_config_c4_sampled_parity(M, oracle_mod):
     E = g.n_edges
     full = M.comine(g, tree)
     assert all(x >= 0 for x in full) and sum(full) > 0
-    for a in (E // 3, (7 * E) // 10):
-        rng = (a, a + 1500)
-        exp = oracle_mod.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=rng)
-        assert M.comine(g, tree, rng) == exp
-        assert M.mine_independent(g, tree, rng) == exp
+    stride = E // 32
+    ranges = [(i * stride + stride // 2, i * stride + stride // 2 + 64) for i in range(32)]
+    heavy, sizes = _heaviest_roots(src, dst, t, cfg.delta, 8)
+    assert min(sizes) > 50                                   # they are hub roots
+    ranges += [(r, r + 1) for r in heavy]
+    # the oracle's ids are its own (t, input rank) sort; the GPU's are the same order (R1)
+    per, _, _ = oracle_mod.backtrack_ranges(src, dst, t, V, cfg.group(), cfg.delta, ranges)
+    for rg, exp in zip(ranges, per):
+        assert M.comine(g, tree, rg) == exp, rg
+    assert sum(sum(x) for x in per[32:]) > 0                 # the heavy roots have matches
+    assert M.mine_independent(g, tree, ranges[5]) == per[5]
     cut = E // 2
     halves = [M.comine(g, tree, (0, cut)), M.comine(g, tree, (cut, E))]
     assert [x + y for x, y in zip(*halves)] == full
+    os.environ["MAYURA_KERNEL"] = "hybrid"
+    try:
+        assert M.comine(g, tree) == full
+    finally:
+        del os.environ["MAYURA_KERNEL"]
+
+
+@pytest.mark.slow
+def test_config_c5_sampled_parity_full_size(M, oracle_mod):
+    """C5 at full size (500 M edges, 10 M vertices, planted AML patterns, 8 motifs): the whole
+    graph on the GPU (one replica, ~50 GB), exact per-motif parity on 4 evenly spaced 2,000-root
+    ranges against the oracle, and the planted lower bounds."""
+    cfg = synth.CONFIGS["C5"]
+    src, dst, t, V = cfg.graph()
+    g = M.Graph(src, dst, t, V, device=0)
+    tree = M.MGTree(cfg.group(), cfg.delta)
+    E = g.n_edges
+    full = M.comine(g, tree)
+    ranges = [(i * (E // 4) + E // 8, i * (E // 4) + E // 8 + 2000) for i in range(4)]
+    per, _, _ = oracle_mod.backtrack_ranges(src, dst, t, V, cfg.group(), cfg.delta, ranges)
+    for rg, exp in zip(ranges, per):
+        assert M.comine(g, tree, rg) == exp, rg
+    # planted patterns: every planted instance is a match (lower bounds; the background adds more)
+    planted_fan_out = sum(v for k, v in synth.plant_aml(cfg.planted, cfg.n_vertices, cfg.span, cfg.delta,
+                                                           cfg.seed)[3]["fan_out"].items())
+    assert full[cfg.motifs.index("fan_out3")] >= planted_fan_out
 
 
 def test_config_c5s_full_parity(M, oracle_mod):

@@ -19,14 +19,13 @@ echo "bench C2 rc=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_C4_${TAG}.csv python bench.py --profile --steps 3 --warmup 3 > /dev/null 2>&1
 echo "ncu launches rc=$?"
-K='regex:"window_end|flat_win|flat_entry|expand_kernel|long_kernel|comine_lane"'
 for CC in all none; do
   timeout 1200 ncu --set full --clock-control none --cache-control $CC --import-source on \
-    -k regex:"window_end|flat_win|flat_entry|expand_kernel|long_kernel|comine_lane" -s 4 -c 4 \
+    -k regex:"window_end|wdfs_kernel" -s 2 -c 2 \
     -o gpurun_out/prof_C4_${CC}_${TAG} -f python bench.py --profile --steps 1 --warmup 1 > gpurun_out/ncu_${CC}.log 2>&1
   echo "ncu full C4 cache=$CC rc=$?"
   ncu -i gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep --page raw --csv > gpurun_out/ncu_full_C4_${CC}_${TAG}_raw.csv 2>/dev/null
-  ncu -i gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep --page source --csv -k regex:comine_lane > gpurun_out/ncu_src_C4_${CC}_${TAG}.csv 2>/dev/null
-  [ $(stat -c %s gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep) -gt 25000000 ] && rm -f gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep
+  ncu -i gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep --page source --csv --print-source sass -k regex:wdfs > gpurun_out/ncu_src_C4_${CC}_${TAG}.csv 2>/dev/null
+  [ -f gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep ] && [ $(stat -c %s gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep) -gt 25000000 ] && rm -f gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep
 done
 du -sh gpurun_out

@@ -167,19 +167,26 @@ mayura_status mayura_mine_independent(mayura_graph g, mayura_mgtree m, uint64_t 
 
 /* mayura_comine_ex -- mayura_comine (independent == 0) or mayura_mine_independent
  * (independent != 0), additionally recording the caller's cudaEvent_t `mid_event`
- * (may be NULL) on `cuda_stream` after the window-end kernel and before the first
- * co-mining kernel, so the caller can time the co-mining kernel alone with events
- * on the launching stream. */
+ * (may be NULL) on `cuda_stream` between the query's set-up and its co-mining kernels:
+ * after window_end_kernel (warp / hybrid / lane / bfs forms), or after the counts memset
+ * in the flat form (which has no window-end kernel: its level-0 pass computes the window
+ * ends itself, so there the interval after the event includes step a2).  The caller times
+ * the co-mining pass with events on the launching stream. */
 mayura_status mayura_comine_ex(mayura_graph g, mayura_mgtree m, uint64_t root_begin,
                                uint64_t root_end, void *cuda_stream, uint64_t *counts_out,
                                int counts_on_device, int independent, void *mid_event);
 
-/* mayura_comine_stats -- the same search in an instrumented kernel (not for timing):
+/* mayura_comine_stats -- the same search in an instrumented kernel (not for timing; the
+ * instrumented depth-first lane kernel, after the breadth-first level in the hybrid form):
  * stats_out[0..7] = roots visited (non-self-loop), search-tree nodes expanded (partial
- * matches whose children were examined), windows located, window entries examined,
- * search probes (32-ary sample loads), batches loaded, algorithmic bytes B_alg
- * (DESIGN.md §6), matches counted; stats_out[8..9] = load-balance offloads (a warp
- * split the rest of a long window into queued contexts), contexts processed.
+ * matches whose children were examined), windows located, in-window entries examined,
+ * binary-search probes (window starts located by search), lane iterations that loaded an
+ * entry, implementation bytes, matches counted; stats_out[8..9] = load-
+ * balance offloads (partial matches handed to a warp's task stack), contexts processed.
+ * Roots, nodes, windows, entries and matches are properties of the search tree, identical
+ * in every kernel form; bench.py computes SURVEY.md's B_alg from them.  With the
+ * environment variable MAYURA_WDFS_STATS=1 (and the warp form) the instrumented warp kernel
+ * runs instead and reuses the fields for its round counters (tools/wdfs_stats.py).
  * stats_out must hold 10 entries.  Host output; synchronises. */
 mayura_status mayura_comine_stats(mayura_graph g, mayura_mgtree m, uint64_t root_begin,
                                   uint64_t root_end, int independent, uint64_t *stats_out);
@@ -225,18 +232,23 @@ mayura_status mayura_comine_heuristic(mayura_graph g, mayura_mgtree m, int *use_
 
 /* ------------------------------------------------------------ multi-GPU ---
  * mayura_partition_roots -- split [0, E) into n_parts contiguous root ranges
- * (timestamp ranges) of balanced estimated work (proxy: 1 + number of edges in
- * the root's window (t_r, t_r + delta]).  Deterministic, host-only, works on
- * host-only graphs.  bounds_out: n_parts + 1 entries, bounds_out[0] = 0,
- * bounds_out[n_parts] = E, non-decreasing. */
+ * (timestamp ranges) of balanced estimated work.  Proxy work of root r:
+ * p(r) = 1 + min(s_r, 65535)^2, s_r = entries with t_r < t <= t_r + delta in the four
+ * adjacency lists at the root's endpoints (out(src), in(dst), out(dst), in(src)); cut p
+ * at the first root whose proxy prefix sum reaches floor(total * p / n_parts).
+ * Deterministic: host arithmetic for host-only graphs, the same integer arithmetic on
+ * the GPU for device-built graphs (identical bounds, tests/test_gpu_parity.py).
+ * bounds_out: n_parts + 1 entries, bounds_out[0] = 0, bounds_out[n_parts] = E,
+ * non-decreasing.  Errors: E_INVALID (NULL, n_parts == 0, delta < 0), E_CUDA. */
 mayura_status mayura_partition_roots(mayura_graph g, int64_t delta, uint32_t n_parts,
                                      uint64_t *bounds_out);
 
 /* Kernel form mayura_comine uses for this graph: "flat" (level-synchronous,
- * entry-parallel; the default when the graph arrays fit in L2), "hybrid" (one breadth-first
- * level + the depth-first lane kernel; the default otherwise), or "lane" / "bfs" when forced
- * with the MAYURA_KERNEL environment variable; "none" for NULL or host-only graphs.  All
- * forms return identical counts.  Static string. */
+ * entry-parallel; the default when the graph arrays fit in L2), "warp" (the warp-synchronous
+ * depth-first kernel over a shared-memory stack of window pieces; the default otherwise), or
+ * "hybrid" / "lane" / "bfs" / "mixed" when forced with the MAYURA_KERNEL environment
+ * variable; "none" for NULL or host-only graphs.  All forms return identical counts.
+ * Static string. */
 const char *mayura_kernel_form(mayura_graph g);
 
 /* Form the last mayura_enumerate call on this graph took (enumeration row):
@@ -249,7 +261,7 @@ const char *mayura_enum_form(mayura_graph g);
 /* Thread-local message for the last failing call on this thread ("" if none). */
 const char *mayura_last_error(void);
 
-/* Library version string, e.g. "mayura-b200 0.2 sm_100a". */
+/* Library version string, e.g. "mayura-b200 0.3 sm_100a". */
 const char *mayura_version(void);
 
 /* Number of the library's own (hand-written) kernel launches enqueued so far in this

@@ -20,7 +20,7 @@ using namespace mayura;
 
 extern "C" const char *mayura_last_error(void) { return g_last_error.c_str(); }
 
-extern "C" const char *mayura_version(void) { return "mayura-b200 0.2 sm_100a"; }
+extern "C" const char *mayura_version(void) { return "mayura-b200 0.3 sm_100a"; }
 
 namespace mayura {
 uint64_t launch_count();

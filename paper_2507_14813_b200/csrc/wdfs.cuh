@@ -90,7 +90,7 @@ __host__ __device__ inline size_t off_stk(uint32_t nn, uint32_t ng, uint32_t ns,
     return lane::align16(off_cnt(nn, ng, ns) + (lanecnt ? (size_t)ns * kWB * 4 : 0));
 }
 __host__ __device__ inline size_t smem_bytes(uint32_t nn, uint32_t ng, uint32_t ns, bool lanecnt, int maxv, int cap) {
-    return off_stk(nn, ng, ns, lanecnt) + (size_t)kWarps * ((6 + maxv) * cap + 2 * (10 + maxv) * 32) * 4;
+    return off_stk(nn, ng, ns, lanecnt) + (size_t)kWarps * ((6 + maxv) * cap + (10 + maxv) * 32) * 4;
 }
 
 // Length of a window: entries [lo, lo + n) are the entries of list `ent` from lo with time
@@ -214,9 +214,8 @@ __device__ __noinline__ void reload(uint32_t *stk, uint32_t m, const uint32_t *s
     __syncwarp();
 }
 
-// Per-warp staging areas (shared memory, SoA, 32 slots = one per lane) of the partial matches to
-// expand next: the children found by a round's first / second slots (or the items just taken),
-// so no partial match is held in registers across the round.  Words: 0 node | c_out << 31,
+// Per-warp staging area (shared memory, SoA, 32 slots = one per lane) of the children found by a
+// round's second slots, expanded after the first slots' ones.  Words: 0 node | c_out << 31,
 // 1 tr_prev, 2 h, 3 root, 4..7 P, 8 c_lo, 9 c_end, 10.. m2g[MAXV]
 template <int MAXV>
 struct Stage {
@@ -343,7 +342,7 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
     const uint32_t tid = threadIdx.x, lane_id = tid & 31;
     constexpr int F = Piece<MAXV>::F;
     constexpr int SF = Stage<MAXV>::F;
-    uint32_t *stk = reinterpret_cast<uint32_t *>(smem + w.o_stk) + (size_t)(tid >> 5) * (F * CAP + 2 * SF * 32);
+    uint32_t *stk = reinterpret_cast<uint32_t *>(smem + w.o_stk) + (size_t)(tid >> 5) * (F * CAP + SF * 32);
     uint32_t *sg = stk + F * CAP;
     uint32_t *sp = w.spill + (size_t)(blockIdx.x * kWarps + (tid >> 5)) * w.spill_cap * F;
     __shared__ uint32_t s_gw[lane::kGwMax];
@@ -407,11 +406,12 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
     uint32_t cb = 0, cl = 0;   // warp-uniform item chunk
     bool items_left = true;
     uint32_t *own = s_own[tid >> 5];
-    uint32_t *sga = sg, *sgb = sg + Stage<MAXV>::F * 32;  // staging of the first / second slots' children
+    uint32_t *sgb = sg;  // staging of the second slot's children
 
     // Test the candidate entry of one slot: window entry `at` of piece `pi`.  Completions are
     // counted; an inner hit fills y (the child partial match) and its continuation window.
-    auto test_slot = [&](uint32_t pi, uint32_t at, uint32_t *sgx) -> bool {
+    auto test_slot = [&](uint32_t pi, uint32_t at, bfs::PM<MAXV> &y, uint32_t &y_lo, uint32_t &y_end,
+                         bool &y_out) -> bool {
         const uint32_t g = stk[0 * CAP + pi];
         const uint32_t p0 = stk[1 * CAP + pi];
         const uint32_t pos = p0 + at;
@@ -463,8 +463,7 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
         if (dn.flags & NODE_COMPLETION) cnt_add(dn.slot);
         if (STATS) st[ST_MATCHES] += (dn.flags & NODE_COMPLETION) ? 1 : 0;
         if (!(dn.flags & NODE_INNER)) return false;
-        // the child partial match (Algo 3 l.665-669), staged in shared memory for open_push
-        bfs::PM<MAXV> y;
+        // the child partial match (Algo 3 l.665-669)
 #pragma unroll
         for (int k = 0; k < MAXV; k++) y.m2g[k] = m2g[k];
         if (dn.n_new == 2) {
@@ -479,7 +478,9 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
         y.h = h;
         y.root = stk[5 * CAP + pi];
         y.P = P;
-        stage_put<MAXV>(sgx, lane_id, y, glob ? 0u : pos + 1, glob ? 0u : p0 + stk[2 * CAP + pi], out);
+        y_lo = glob ? 0u : pos + 1;
+        y_end = glob ? 0u : p0 + stk[2 * CAP + pi];
+        y_out = out;
         if (STATS) st[ST_NODES]++;
         return true;
     };
@@ -504,7 +505,10 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
         incl1 += tot0;
         const uint32_t tot = __shfl_sync(kFull, incl1, 31);
 
-        bool has = false, has_b = false;  // this lane staged a partial match in staging area a / b
+        bfs::PM<MAXV> x;   // this lane's new partial match: an item, or the first slot's child
+        bool has = false, has_b = false;
+        uint32_t c_lo = 0, c_end = 0;  // a child's continuation window on its parent's list
+        bool c_out = false;
         if (top == 0 && sp_top > 0) {
             // ---- the stack ran empty: bring back the most recently spilled pieces (depth first)
             const uint32_t m = min(sp_top, (uint32_t)CAP / 2);
@@ -538,7 +542,6 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
             cb += take;
             cl -= take;
             if (lane_id < take) {
-                bfs::PM<MAXV> x;
                 if (w.direct) {  // a root edge: count the root node's completion, expand it if inner
                     const uint32_t r = p.r0 + item;
                     if (bfs::load_root<MAXV>(p, r, x)) {
@@ -551,7 +554,6 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
                 } else {  // a light root (its completion was counted by the breadth-first level)
                     has = bfs::load_root<MAXV>(p, __ldg(p.light + (item - n_pm)), x);
                 }
-                if (has) stage_put<MAXV>(sga, lane_id, x, 0u, 0u, false);
             }
             if (STATS && lane_id == 0) st[ST_ROOTS] += take;
         } else {
@@ -574,8 +576,12 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
             const uint32_t hb = mhi & le;
             const uint32_t sb = hb ? 63 - __clz(hb) : 31 - __clz(mlo | 1u);
             const bool act_a = lane_id < T, act_b = lane_id + 32 < T;
-            if (act_a) has = test_slot(top - 1 - own[sa], lane_id - sa, sga);
-            if (act_b) has_b = test_slot(top - 1 - own[sb], lane_id + 32 - sb, sgb);
+            uint32_t b_lo = 0, b_end = 0;
+            bool b_out = false;
+            bfs::PM<MAXV> yb;
+            if (act_a) has = test_slot(top - 1 - own[sa], lane_id - sa, x, c_lo, c_end, c_out);
+            if (act_b) has_b = test_slot(top - 1 - own[sb], lane_id + 32 - sb, yb, b_lo, b_end, b_out);
+            if (has_b) stage_put<MAXV>(sgb, lane_id, yb, b_lo, b_end, b_out);
             if (STATS && lane_id == 0) {
                 st[ST_BATCHES]++;
                 st[ST_PROBES] += T;
@@ -595,14 +601,14 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
         // ---- the new partial matches' windows go on top of the stack (depth first): the first
         // slot's children (or the items) from registers, then the second slot's from staging
         for (int half = 0; half < 2; half++) {
-            const bool hv = half ? has_b : has;
-            if (!__any_sync(kFull, hv)) continue;
-            bfs::PM<MAXV> x;
-            uint32_t c_lo = 0, c_end = 0;  // a child's continuation window on its parent's list
-            bool c_out = false;
-            if (hv) stage_get<MAXV>(half ? sgb : sga, lane_id, x, c_lo, c_end, c_out, s_nodes);
-            open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, hv, x, c_lo, c_end, c_out,
-                                             my_cnt, s_tot, st);
+            if (half == 1) {
+                if (!__any_sync(kFull, has_b)) break;
+                has = has_b;
+                if (has_b) stage_get<MAXV>(sgb, lane_id, x, c_lo, c_end, c_out, s_nodes);
+            }
+            if (__any_sync(kFull, has))
+                open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, has, x, c_lo, c_end, c_out,
+                                                 my_cnt, s_tot, st);
         }
     }
 

@@ -32,7 +32,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 KERNELS = {"flat": "co-mining pass (flat form): per MG-Tree level flat::flat_win_kernel + flat::flat_entry_kernel",
-           "hybrid": "co-mining pass (hybrid form): bfs::expand_kernel + bfs::long_kernel + lane::comine_lane_kernel"}
+           "warp": "co-mining pass (warp form): wdfs::wdfs_kernel (warp-synchronous depth-first, lane per window entry)",
+           "hybrid": "co-mining pass (hybrid form): bfs::expand_kernel + bfs::long_kernel + wdfs::wdfs_kernel"}
 METRIC = "motif-group co-mining time (s) and root edges/s at 1/2/4/8 B200; HBM GB/s frac"
 UNIT = "root edges/s"
 
@@ -40,7 +41,7 @@ UNIT = "root edges/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["mayura", "reference"], default="mayura")
     ap.add_argument("--config", default="C4",
@@ -450,15 +451,20 @@ def main():
     n_range = re_ - rb
     b_alg = 16 * n_range + 8 * (st["entries"] + st["windows"])
     achieved = b_alg / (ms_kern * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_info = None, None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         tr = json.load(open(prof)).get(cfg.name)
-        if tr:
+        if tr and world == 1:
             traffic = tr.get("dram_bytes_per_launch")
+            traffic_info = {"warm": tr.get("dram_bytes_per_launch_warm"), "capture": tr.get("tag"),
+                            "kernels": tr.get("kernels"), "over_bytes_alg": traffic / b_alg if b_alg else None,
+                            "note": "committed ncu --set full capture of one pass of this workload "
+                                    "(profiles/ncu_traffic.json): cold = caches flushed before each replay, "
+                                    "warm = --cache-control none"}
     form = M.mayura_kernel_form(g.handle)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic,
+                "traffic": traffic, "traffic_info": traffic_info,
                 "kernel": KERNELS.get(form, form), "kernel_form": form,
                 "kernel_ms": ms_kern,
                 "window_end_kernel_ms": ms_win, "bytes_alg_per_launch": b_alg,

@@ -24,7 +24,8 @@ for CC in all none; do
     -k regex:"window_end|wdfs_kernel" -s 2 -c 2 \
     -o gpurun_out/prof_C4_${CC}_${TAG} -f python bench.py --profile --steps 1 --warmup 1 > gpurun_out/ncu_${CC}.log 2>&1
   echo "ncu full C4 cache=$CC rc=$?"
-  ncu -i gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep --page raw --csv > gpurun_out/ncu_full_C4_${CC}_${TAG}_raw.csv 2>/dev/null
+  SFX=$([ "$CC" == "none" ] && echo "_warm" || echo "")
+  ncu -i gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep --page raw --csv > gpurun_out/prof_C4_${TAG}${SFX}_raw.csv 2>/dev/null
   ncu -i gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep --page source --csv --print-source sass -k regex:wdfs > gpurun_out/ncu_src_C4_${CC}_${TAG}.csv 2>/dev/null
   [ -f gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep ] && [ $(stat -c %s gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep) -gt 25000000 ] && rm -f gpurun_out/prof_C4_${CC}_${TAG}.ncu-rep
 done

@@ -84,23 +84,35 @@ def main():
     rec["roots_per_s_8gpu"] = E / (max(per) * 1e-3)
     rec["rank_balance_max_over_mean"] = max(per) / (sum(per) / 8)
     rec["ranks_sum_equals_full"] = tot == full
-    # parity on sampled root ranges
+    # the hybrid form (breadth-first level + warp kernel) on the whole graph, for the form choice
+    os.environ["MAYURA_KERNEL"] = "hybrid"
+    run(0, E)
+    hms, _ = timed(lambda: run(0, E), 3)
+    rec["hybrid_ms_1gpu"] = hms
+    rec["hybrid_equal"] = counts.cpu().tolist() == full
+    del os.environ["MAYURA_KERNEL"]
+    rec["kernel_form"] = M.mayura_kernel_form(g.handle)
+    # parity on 8 evenly spaced 2,000-root ranges, one oracle graph build
     samples = []
-    for a in (() if no_oracle else (E // 3, (2 * E) // 3)):
-        rng = (a, a + 4000)
-        t0 = time.time()
-        exp = oracle.backtrack(src, dst, t, V, cfg.group(), cfg.delta, root_range=rng)
-        dt = time.time() - t0
-        run(*rng)
-        got = counts.cpu().tolist()
-        samples.append({"range": rng, "exact": got == exp, "oracle_s": dt, "oracle_roots_per_s": 4000 / dt})
+    if not no_oracle:
+        rngs = [(i * (E // 8) + E // 16, i * (E // 8) + E // 16 + 2000) for i in range(8)]
+        per_o, build_s, mine_s = oracle.backtrack_ranges(src, dst, t, V, cfg.group(), cfg.delta, rngs)
+        for rng, exp in zip(rngs, per_o):
+            run(*rng)
+            samples.append({"range": rng, "exact": counts.cpu().tolist() == exp})
+        rec["oracle_build_s"] = build_s
+        rec["oracle_roots_per_s"] = 16000 / mine_s
     rec["sampled_parity"] = samples
     lb = _planted_lower_bounds(planted)
     rec["planted_lower_bounds_hold"] = all(rec["counts"][n] >= lb[n] for n in lb)
     rec["planted"] = {kk: {str(a): b for a, b in v.items()} for kk, v in planted.items()}
     st = M.comine_stats(g, tree)
     rec["search_stats"] = st
-    rec["bytes_alg_per_root"] = st["bytes_alg"] / E
+    b_alg = 16 * E + 8 * (st["entries"] + st["windows"])  # SURVEY.md:540
+    rec["bytes_alg_per_root"] = b_alg / E
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    rec["roofline_frac_1gpu"] = b_alg / (ms * 1e-3) / 1e9 / peak
     print(json.dumps(rec))
     os.makedirs(os.path.dirname(out_path) or ".", exist_ok=True)
     with open(out_path, "w") as f:

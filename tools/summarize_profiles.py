@@ -116,21 +116,30 @@ def main():
                     if k in d:
                         lines.append("| %s (`%s`) | %s %s |" % (name, k, d[k], u.get(k, "")))
                 lines.append("")
-            # DRAM traffic of one co-mining pass (all captured kernels of one step) for bench.py
-            recs = ncu_raw(rp)
-            if recs:
-                tot = 0.0
-                names = []
-                for d, u in recs:
+            # DRAM traffic of one co-mining pass for bench.py: the kernels bench.py's achieved
+            # bandwidth covers (the events after mid_event: window_end_kernel excluded)
+            def traffic(path):
+                tot, names = 0.0, []
+                for d, u in ncu_raw(path):
+                    if "window_end_kernel" in d.get("Kernel Name", ""):
+                        continue
                     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                         v = float(d.get(k, "0").replace(",", "") or 0)
                         tot += v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u.get(k, "byte"), 1)
                     names.append(d.get("Kernel Name", "?")[:80])
+                return tot, names
+            tot, names = traffic(rp)
+            if names:
                 tj = os.path.join(PROF, "ncu_traffic.json")
                 allt = json.load(open(tj)) if os.path.exists(tj) else {}
                 allt[c] = {"dram_bytes_per_launch": tot, "kernels": names, "tag": tag,
-                           "note": "dram__bytes_read.sum + dram__bytes_write.sum summed over the kernels of one "
-                                   "co-mining pass, ncu --set full (cold L2 per replay)"}
+                           "note": "dram__bytes_read.sum + dram__bytes_write.sum summed over the co-mining kernels "
+                                   "of one pass (window_end_kernel excluded, as in bench.py's achieved), "
+                                   "ncu --set full, default --cache-control all (caches flushed before each replay)"}
+                wp = os.path.join(OUT, "prof_%s_%s_warm_raw.csv" % (c, tag))
+                if os.path.exists(wp):
+                    allt[c]["dram_bytes_per_launch_warm"] = traffic(wp)[0]
+                    allt[c]["note_warm"] = "the same capture with --cache-control none (caches kept across replays)"
                 json.dump(allt, open(tj, "w"), indent=1)
         with open(os.path.join(PROF, "%s_%s.md" % (tag, c)), "w") as f:
             f.write("\n".join(lines) + "\n")

@@ -82,9 +82,14 @@ struct WParams {
     uint32_t ent_len;        // adjacency entries (E + V, sentinels included) -- WDFS_CHECK only
 };
 
-__host__ __device__ inline size_t off_cnt(uint32_t nn, uint32_t ng, uint32_t ns) {
+// dynamic shared memory: nodes | groups | slot totals (u64) | node info | group info | group wants |
+// lane counters | per-warp stacks + staging
+__host__ __device__ inline size_t off_info(uint32_t nn, uint32_t ng, uint32_t ns) {
     return lane::align16((size_t)nn * sizeof(lane::LNode)) + lane::align16((size_t)ng * sizeof(DGroup)) +
            lane::align16((size_t)ns * 8);
+}
+__host__ __device__ inline size_t off_cnt(uint32_t nn, uint32_t ng, uint32_t ns) {
+    return off_info(nn, ng, ns) + lane::align16((size_t)nn * 4) + 2 * lane::align16((size_t)ng * 4);
 }
 __host__ __device__ inline size_t off_stk(uint32_t nn, uint32_t ng, uint32_t ns, bool lanecnt) {
     return lane::align16(off_cnt(nn, ng, ns) + (lanecnt ? (size_t)ns * kWB * 4 : 0));
@@ -212,6 +217,25 @@ __device__ __noinline__ void reload(uint32_t *stk, uint32_t m, const uint32_t *s
         stk[f * CAP + i] = sp[(size_t)(sp_top - m + i) * F + f];
     }
     __syncwarp();
+}
+
+// Packed table words (wdfs_kernel prologue): per group, kind | SIMD child lookup possible | a
+// child locates a window from the entry's successor pointers | first child << 16; per node,
+// completion slot | completion | inner | n_new << 18 | nv << 24.
+constexpr uint32_t GI_KIND = 3u, GI_SIMD = 4u, GI_NEEDP = 8u;
+constexpr uint32_t NI_COMPLETION = 1u << 16, NI_INNER = 1u << 17;
+__device__ __forceinline__ uint32_t group_info(const DGroup &G, const lane::LNode *nodes) {
+    bool np = false;
+    for (uint32_t ch = G.child_begin; ch < G.child_end; ch++) {
+        const lane::LNode dn = nodes[ch];
+        np = np || ((dn.flags & NODE_INNER) && (dn.flags & NODE_NEEDP));
+    }
+    const bool simd = G.child_end - G.child_begin <= 4;
+    return (uint32_t)G.kind | (simd ? GI_SIMD : 0u) | (np ? GI_NEEDP : 0u) | ((uint32_t)G.child_begin << 16);
+}
+__device__ __forceinline__ uint32_t node_info(const lane::LNode &n) {
+    return (uint32_t)(n.slot & 0xFFFFu) | ((n.flags & NODE_COMPLETION) ? NI_COMPLETION : 0u) |
+           ((n.flags & NODE_INNER) ? NI_INNER : 0u) | ((uint32_t)(n.n_new & 3u) << 18) | ((uint32_t)n.nv << 24);
 }
 
 // Per-warp staging area (shared memory, SoA, 32 slots = one per lane) of the children found by a
@@ -345,24 +369,18 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
     uint32_t *stk = reinterpret_cast<uint32_t *>(smem + w.o_stk) + (size_t)(tid >> 5) * (F * CAP + SF * 32);
     uint32_t *sg = stk + F * CAP;
     uint32_t *sp = w.spill + (size_t)(blockIdx.x * kWarps + (tid >> 5)) * w.spill_cap * F;
-    __shared__ uint32_t s_gw[lane::kGwMax];
     __shared__ uint32_t s_pref[bfs::kStripes + 1];
-    __shared__ uint32_t s_np[lane::kGwMax / 32];  // bit g: a child of group g needs P (NODE_NEEDP)
     __shared__ uint32_t s_own[kWarps][64];        // per warp: round slot -> index of the piece starting there
+    // Packed per-node / per-group words (one 32-bit shared load per candidate instead of the 12- and
+    // 8-byte table rows and their byte extraction) and the groups' packed child wants
+    uint32_t *s_ninfo = reinterpret_cast<uint32_t *>(smem + off_info(p.n_nodes, p.n_groups, p.n_slots));
+    uint32_t *s_ginfo = s_ninfo + lane::align16((size_t)p.n_nodes * 4) / 4;
+    uint32_t *s_gw = s_ginfo + lane::align16((size_t)p.n_groups * 4) / 4;
     for (uint32_t i = tid; i < p.n_nodes; i += kWB) s_nodes[i] = p.nodes[i];
     for (uint32_t i = tid; i < p.n_groups; i += kWB) s_groups[i] = p.groups[i];
-    for (uint32_t i = tid; i < p.n_groups && i < lane::kGwMax; i += kWB) s_gw[i] = w.gwant[i];
-    if (tid < lane::kGwMax / 32) s_np[tid] = 0;
-    __syncthreads();
-    for (uint32_t g = tid; g < p.n_groups && g < lane::kGwMax; g += kWB) {
-        const DGroup G = p.groups[g];
-        bool np = false;
-        for (uint32_t ch = G.child_begin; ch < G.child_end; ch++) {
-            const lane::LNode dn = p.nodes[ch];
-            np = np || ((dn.flags & NODE_INNER) && (dn.flags & NODE_NEEDP));
-        }
-        if (np) atomicOr(&s_np[g >> 5], 1u << (g & 31));
-    }
+    for (uint32_t i = tid; i < p.n_groups; i += kWB) s_gw[i] = w.gwant[i];
+    for (uint32_t g = tid; g < p.n_groups; g += kWB) s_ginfo[g] = group_info(p.groups[g], p.nodes);
+    for (uint32_t n = tid; n < p.n_nodes; n += kWB) s_ninfo[n] = node_info(p.nodes[n]);
     for (uint32_t i = tid; i < p.n_slots; i += kWB) s_tot[i] = 0;
     if (s_cnt)
         for (uint32_t i = 0; i < p.n_slots; i++) s_cnt[i * kWB + tid] = 0;
@@ -421,14 +439,14 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
                "entry pos %u (p0 %u at %u) kind %u", pos, p0, at, (unsigned)s_groups[g].kind);
         const uint32_t tp = stk[3 * CAP + pi];
         const uint32_t h = stk[4 * CAP + pi];
-        const DGroup G = s_groups[g];
-        const bool glob = GEN && G.kind == ANCHOR_GLOBAL;
+        const uint32_t gi = s_ginfo[g];
+        const bool glob = GEN && (gi & GI_KIND) == ANCHOR_GLOBAL;
         // successor pointers of the entry's edge, loaded with the entry (no extra round trip)
         // when a child of this group locates a window from them
-        const bool needp = G.n_inner && (g >= lane::kGwMax || ((s_np[g >> 5] >> (g & 31)) & 1u));
+        const bool needp = (gi & GI_NEEDP) != 0;
         uint32_t etr, e1, e2 = 0;
         uint4 P = make_uint4(0, 0, 0, 0);
-        const bool out = G.kind == ANCHOR_OUT;
+        const bool out = (gi & GI_KIND) == ANCHOR_OUT;
         if (glob) {
             etr = __ldg(p.tr + pos);
             e1 = __ldg(p.src + pos);
@@ -452,28 +470,29 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
         else
             cls = lane::classify<MAXV>(m2g, e1);
         uint32_t hit = kNone;
-        if (G.child_end - G.child_begin <= 4 && g < lane::kGwMax) {
+        if (gi & GI_SIMD) {
             const uint32_t eq = __vcmpeq4(s_gw[g], cls * 0x01010101u);
-            hit = eq ? G.child_begin + ((__ffs(eq) - 1) >> 3) : kNone;
+            hit = eq ? (gi >> 16) + ((__ffs(eq) - 1) >> 3) : kNone;
         } else {
-            hit = bfs::find_child(s_nodes, G, cls);
+            hit = bfs::find_child(s_nodes, s_groups[g], cls);
         }
         if (!valid || hit == kNone) return false;
-        const lane::LNode dn = s_nodes[hit];
-        if (dn.flags & NODE_COMPLETION) cnt_add(dn.slot);
-        if (STATS) st[ST_MATCHES] += (dn.flags & NODE_COMPLETION) ? 1 : 0;
-        if (!(dn.flags & NODE_INNER)) return false;
+        const uint32_t ni = s_ninfo[hit];
+        if (ni & NI_COMPLETION) cnt_add(ni & 0xFFFFu);
+        if (STATS) st[ST_MATCHES] += (ni & NI_COMPLETION) ? 1 : 0;
+        if (!(ni & NI_INNER)) return false;
         // the child partial match (Algo 3 l.665-669)
+        const uint32_t n_new = (ni >> 18) & 3u, nv = ni >> 24;
 #pragma unroll
         for (int k = 0; k < MAXV; k++) y.m2g[k] = m2g[k];
-        if (dn.n_new == 2) {
-            lane::m2g_set<MAXV>(y.m2g, dn.nv - 2u, e1);
-            lane::m2g_set<MAXV>(y.m2g, dn.nv - 1u, e2);
-        } else if (dn.n_new == 1) {
-            lane::m2g_set<MAXV>(y.m2g, dn.nv - 1u, e1);
+        if (n_new == 2) {
+            lane::m2g_set<MAXV>(y.m2g, nv - 2u, e1);
+            lane::m2g_set<MAXV>(y.m2g, nv - 1u, e2);
+        } else if (n_new == 1) {
+            lane::m2g_set<MAXV>(y.m2g, nv - 1u, e1);
         }
         y.node = hit;
-        y.nv = dn.nv;
+        y.nv = nv;
         y.tr_prev = etr;
         y.h = h;
         y.root = stk[5 * CAP + pi];

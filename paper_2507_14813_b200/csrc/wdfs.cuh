@@ -370,7 +370,6 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
     uint32_t *sg = stk + F * CAP;
     uint32_t *sp = w.spill + (size_t)(blockIdx.x * kWarps + (tid >> 5)) * w.spill_cap * F;
     __shared__ uint32_t s_pref[bfs::kStripes + 1];
-    __shared__ uint32_t s_own[kWarps][64];        // per warp: round slot -> index of the piece starting there
     // Packed per-node / per-group words (one 32-bit shared load per candidate instead of the 12- and
     // 8-byte table rows and their byte extraction) and the groups' packed child wants
     uint32_t *s_ninfo = reinterpret_cast<uint32_t *>(smem + off_info(p.n_nodes, p.n_groups, p.n_slots));
@@ -423,7 +422,6 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
     uint32_t sp_top = 0;       // warp-uniform spilled pieces (global memory)
     uint32_t cb = 0, cl = 0;   // warp-uniform item chunk
     bool items_left = true;
-    uint32_t *own = s_own[tid >> 5];
     uint32_t *sgb = sg;  // staging of the second slot's children
 
     // Test the candidate entry of one slot: window entry `at` of piece `pi`.  Completions are
@@ -506,22 +504,18 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
 
     for (;;) {
         // ---- the top 64 pieces: candidate counts and their running sum (top first); lane l holds
-        // pieces l and l + 32
+        // pieces 2l and 2l + 1 (one prefix sum of the pairs)
         const uint32_t top = ps;
-        const uint32_t pn0 = lane_id < top ? stk[2 * CAP + top - 1 - lane_id] : 0u;
-        const uint32_t pn1 = lane_id + 32 < top ? stk[2 * CAP + top - 33 - lane_id] : 0u;
-        uint32_t incl0 = pn0, incl1 = pn1;
+        const uint32_t i0 = 2 * lane_id, i1 = 2 * lane_id + 1;
+        const uint32_t pn0 = i0 < top ? stk[2 * CAP + top - 1 - i0] : 0u;
+        const uint32_t pn1 = i1 < top ? stk[2 * CAP + top - 1 - i1] : 0u;
+        uint32_t incl1 = pn0 + pn1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v0 = __shfl_up_sync(kFull, incl0, o);
-            const uint32_t v1 = __shfl_up_sync(kFull, incl1, o);
-            if (lane_id >= (uint32_t)o) {
-                incl0 += v0;
-                incl1 += v1;
-            }
+            const uint32_t v = __shfl_up_sync(kFull, incl1, o);
+            if (lane_id >= (uint32_t)o) incl1 += v;
         }
-        const uint32_t tot0 = __shfl_sync(kFull, incl0, 31);
-        incl1 += tot0;
+        const uint32_t incl0 = incl1 - pn1;  // inclusive sums of pieces 2l and 2l + 1
         const uint32_t tot = __shfl_sync(kFull, incl1, 31);
 
         bfs::PM<MAXV> x;   // this lane's new partial match: an item, or the first slot's child
@@ -580,26 +574,27 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
             // ---- this round: T <= 64 entries, two slots per lane (lane and lane + 32), from the top
             // pieces (the last one possibly split)
             const uint32_t T = min(tot, 64u);
-            const uint32_t x0 = incl0 - pn0, x1 = incl1 - pn1;  // first slot of pieces lane, lane+32
-            const bool pc0 = lane_id < top && x0 < T, pc1 = lane_id + 32 < top && x1 < T;
+            const uint32_t x0 = incl0 - pn0, x1 = incl1 - pn1;  // first slot of pieces 2l, 2l + 1
+            const bool pc0 = i0 < top && x0 < T, pc1 = i1 < top && x1 < T;
             const uint32_t lo_c = (pc0 && x0 < 32 ? 1u << x0 : 0u) | (pc1 && x1 < 32 ? 1u << x1 : 0u);
             const uint32_t hi_c = (pc0 && x0 >= 32 ? 1u << (x0 - 32) : 0u) | (pc1 && x1 >= 32 ? 1u << (x1 - 32) : 0u);
             const uint32_t mlo = __reduce_or_sync(kFull, lo_c), mhi = __reduce_or_sync(kFull, hi_c);
-            if (pc0) own[x0] = lane_id;
-            if (pc1) own[x1] = lane_id + 32;
-            __syncwarp();
-            const uint32_t kf = __popc(__ballot_sync(kFull, lane_id < top && incl0 <= T)) +
-                                __popc(__ballot_sync(kFull, lane_id + 32 < top && incl1 <= T));  // taken whole
+            const uint32_t kf = __popc(__ballot_sync(kFull, i0 < top && incl0 <= T)) +
+                                __popc(__ballot_sync(kFull, i1 < top && incl1 <= T));  // taken whole
+            // the contributing pieces are a prefix (0, 1, ...) of the top pieces, one start bit
+            // each: slot j belongs to piece (start bits <= j) - 1, which starts at the highest one
             const unsigned le = (2u << lane_id) - 1u;
-            const uint32_t sa = 31 - __clz((mlo & le) | 1u);  // first slot of slot lane's piece
+            const uint32_t ra = __popc(mlo & le) - 1u;        // piece of slot lane
+            const uint32_t sa = 31 - __clz((mlo & le) | 1u);  // its first slot
             const uint32_t hb = mhi & le;
+            const uint32_t rb = __popc(mlo) + __popc(hb) - 1u;  // piece of slot lane + 32
             const uint32_t sb = hb ? 63 - __clz(hb) : 31 - __clz(mlo | 1u);
             const bool act_a = lane_id < T, act_b = lane_id + 32 < T;
             uint32_t b_lo = 0, b_end = 0;
             bool b_out = false;
             bfs::PM<MAXV> yb;
-            if (act_a) has = test_slot(top - 1 - own[sa], lane_id - sa, x, c_lo, c_end, c_out);
-            if (act_b) has_b = test_slot(top - 1 - own[sb], lane_id + 32 - sb, yb, b_lo, b_end, b_out);
+            if (act_a) has = test_slot(top - 1 - ra, lane_id - sa, x, c_lo, c_end, c_out);
+            if (act_b) has_b = test_slot(top - 1 - rb, lane_id + 32 - sb, yb, b_lo, b_end, b_out);
             if (has_b) stage_put<MAXV>(sgb, lane_id, yb, b_lo, b_end, b_out);
             if (STATS && lane_id == 0) {
                 st[ST_BATCHES]++;
@@ -608,8 +603,8 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
             __syncwarp();
             // ---- pop the pieces taken whole; advance the split one (piece kf)
             if (kf < top && kf < 64) {  // (kf = 64: the 64 examined pieces were all taken whole)
-                const uint32_t xk = kf < 32 ? x0 : x1;
-                if ((kf & 31) == lane_id && xk < T) {
+                const uint32_t xk = (kf & 1) ? x1 : x0;
+                if ((kf >> 1) == lane_id && xk < T) {
                     stk[1 * CAP + top - 1 - kf] += T - xk;
                     stk[2 * CAP + top - 1 - kf] -= T - xk;
                 }

@@ -31,6 +31,10 @@
 
 namespace wdfs {
 
+#ifndef WDFS_SLOTS
+#define WDFS_SLOTS 2  // candidate entries per lane per round
+#endif
+constexpr int kSlots = WDFS_SLOTS;
 #ifndef WDFS_MINB
 #define WDFS_MINB 5  // resident blocks per SM the register allocation targets (96 registers)
 #endif
@@ -95,7 +99,7 @@ __host__ __device__ inline size_t off_stk(uint32_t nn, uint32_t ng, uint32_t ns,
     return lane::align16(off_cnt(nn, ng, ns) + (lanecnt ? (size_t)ns * kWB * 4 : 0));
 }
 __host__ __device__ inline size_t smem_bytes(uint32_t nn, uint32_t ng, uint32_t ns, bool lanecnt, int maxv, int cap) {
-    return off_stk(nn, ng, ns, lanecnt) + (size_t)kWarps * ((6 + maxv) * cap + (10 + maxv) * 32) * 4;
+    return off_stk(nn, ng, ns, lanecnt) + (size_t)kWarps * ((6 + maxv) * cap + (kSlots - 1) * (10 + maxv) * 32) * 4;
 }
 
 // Length of a window: entries [lo, lo + n) are the entries of list `ent` from lo with time
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
     const uint32_t tid = threadIdx.x, lane_id = tid & 31;
     constexpr int F = Piece<MAXV>::F;
     constexpr int SF = Stage<MAXV>::F;
-    uint32_t *stk = reinterpret_cast<uint32_t *>(smem + w.o_stk) + (size_t)(tid >> 5) * (F * CAP + SF * 32);
+    uint32_t *stk = reinterpret_cast<uint32_t *>(smem + w.o_stk) + (size_t)(tid >> 5) * (F * CAP + (kSlots - 1) * SF * 32);
     uint32_t *sg = stk + F * CAP;
     uint32_t *sp = w.spill + (size_t)(blockIdx.x * kWarps + (tid >> 5)) * w.spill_cap * F;
     __shared__ uint32_t s_pref[bfs::kStripes + 1];
@@ -422,7 +426,6 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
     uint32_t sp_top = 0;       // warp-uniform spilled pieces (global memory)
     uint32_t cb = 0, cl = 0;   // warp-uniform item chunk
     bool items_left = true;
-    uint32_t *sgb = sg;  // staging of the second slot's children
 
     // Test the candidate entry of one slot: window entry `at` of piece `pi`.  Completions are
     // counted; an inner hit fills y (the child partial match) and its continuation window.
@@ -503,23 +506,35 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
     };
 
     for (;;) {
-        // ---- the top 64 pieces: candidate counts and their running sum (top first); lane l holds
-        // pieces 2l and 2l + 1 (one prefix sum of the pairs)
+        // ---- the top 32 * kSlots pieces: candidate counts and their running sum (top first); lane l
+        // holds pieces kSlots * l + i (one prefix sum of the per-lane sums)
         const uint32_t top = ps;
-        const uint32_t i0 = 2 * lane_id, i1 = 2 * lane_id + 1;
-        const uint32_t pn0 = i0 < top ? stk[2 * CAP + top - 1 - i0] : 0u;
-        const uint32_t pn1 = i1 < top ? stk[2 * CAP + top - 1 - i1] : 0u;
-        uint32_t incl1 = pn0 + pn1;
+        uint32_t pn[kSlots], incl[kSlots];
+        uint32_t lsum = 0;
+#pragma unroll
+        for (int i = 0; i < kSlots; i++) {
+            const uint32_t idx = kSlots * lane_id + i;
+            pn[i] = idx < top ? stk[2 * CAP + top - 1 - idx] : 0u;
+            lsum += pn[i];
+        }
+        uint32_t linc = lsum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(kFull, incl1, o);
-            if (lane_id >= (uint32_t)o) incl1 += v;
+            const uint32_t v = __shfl_up_sync(kFull, linc, o);
+            if (lane_id >= (uint32_t)o) linc += v;
         }
-        const uint32_t incl0 = incl1 - pn1;  // inclusive sums of pieces 2l and 2l + 1
-        const uint32_t tot = __shfl_sync(kFull, incl1, 31);
-
+        {
+            uint32_t acc = linc - lsum;
+#pragma unroll
+            for (int i = 0; i < kSlots; i++) {
+                acc += pn[i];
+                incl[i] = acc;  // inclusive sum up to piece kSlots * l + i
+            }
+        }
+        const uint32_t tot = __shfl_sync(kFull, linc, 31);
         bfs::PM<MAXV> x;   // this lane's new partial match: an item, or the first slot's child
-        bool has = false, has_b = false;
+        bool has = false;
+        uint32_t hmask = 0;  // bit s: slot s (>= 1) staged a child
         uint32_t c_lo = 0, c_end = 0;  // a child's continuation window on its parent's list
         bool c_out = false;
         if (top == 0 && sp_top > 0) {
@@ -571,40 +586,60 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
             if (STATS && lane_id == 0) st[ST_ROOTS] += take;
         } else {
             if (top == 0) break;  // no items left, nothing stacked or spilled
-            // ---- this round: T <= 64 entries, two slots per lane (lane and lane + 32), from the top
-            // pieces (the last one possibly split)
-            const uint32_t T = min(tot, 64u);
-            const uint32_t x0 = incl0 - pn0, x1 = incl1 - pn1;  // first slot of pieces 2l, 2l + 1
-            const bool pc0 = i0 < top && x0 < T, pc1 = i1 < top && x1 < T;
-            const uint32_t lo_c = (pc0 && x0 < 32 ? 1u << x0 : 0u) | (pc1 && x1 < 32 ? 1u << x1 : 0u);
-            const uint32_t hi_c = (pc0 && x0 >= 32 ? 1u << (x0 - 32) : 0u) | (pc1 && x1 >= 32 ? 1u << (x1 - 32) : 0u);
-            const uint32_t mlo = __reduce_or_sync(kFull, lo_c), mhi = __reduce_or_sync(kFull, hi_c);
-            const uint32_t kf = __popc(__ballot_sync(kFull, i0 < top && incl0 <= T)) +
-                                __popc(__ballot_sync(kFull, i1 < top && incl1 <= T));  // taken whole
-            // the contributing pieces are a prefix (0, 1, ...) of the top pieces, one start bit
-            // each: slot j belongs to piece (start bits <= j) - 1, which starts at the highest one
+            // ---- this round: T <= 32 * kSlots entries, kSlots slots per lane (lane + 32 s), from the
+            // top pieces (the last one possibly split)
+            const uint32_t T = min(tot, 32u * kSlots);
+            uint32_t xs[kSlots], m[kSlots], kf = 0;
+#pragma unroll
+            for (int wv = 0; wv < kSlots; wv++) {
+                uint32_t c = 0;
+#pragma unroll
+                for (int i = 0; i < kSlots; i++) {
+                    xs[i] = incl[i] - pn[i];  // first slot of piece kSlots * l + i
+                    const bool pc = kSlots * lane_id + i < top && xs[i] < T;
+                    if (pc && (xs[i] >> 5) == (uint32_t)wv) c |= 1u << (xs[i] & 31);
+                }
+                m[wv] = __reduce_or_sync(kFull, c);
+            }
+#pragma unroll
+            for (int i = 0; i < kSlots; i++)
+                kf += __popc(__ballot_sync(kFull, kSlots * lane_id + i < top && incl[i] <= T));  // taken whole
+            // the contributing pieces are a prefix (0, 1, ...) of the top pieces, one start bit each:
+            // slot j belongs to piece (start bits <= j) - 1, which starts at the highest one
             const unsigned le = (2u << lane_id) - 1u;
-            const uint32_t ra = __popc(mlo & le) - 1u;        // piece of slot lane
-            const uint32_t sa = 31 - __clz((mlo & le) | 1u);  // its first slot
-            const uint32_t hb = mhi & le;
-            const uint32_t rb = __popc(mlo) + __popc(hb) - 1u;  // piece of slot lane + 32
-            const uint32_t sb = hb ? 63 - __clz(hb) : 31 - __clz(mlo | 1u);
-            const bool act_a = lane_id < T, act_b = lane_id + 32 < T;
-            uint32_t b_lo = 0, b_end = 0;
-            bool b_out = false;
-            bfs::PM<MAXV> yb;
-            if (act_a) has = test_slot(top - 1 - ra, lane_id - sa, x, c_lo, c_end, c_out);
-            if (act_b) has_b = test_slot(top - 1 - rb, lane_id + 32 - sb, yb, b_lo, b_end, b_out);
-            if (has_b) stage_put<MAXV>(sgb, lane_id, yb, b_lo, b_end, b_out);
+            uint32_t before = 0, last = 0;  // start bits in the words below; highest start slot below
             if (STATS && lane_id == 0) {
                 st[ST_BATCHES]++;
                 st[ST_PROBES] += T;
             }
+#pragma unroll
+            for (int sl = 0; sl < kSlots; sl++) {
+                const uint32_t up = m[sl] & le;
+                const uint32_t r = before + __popc(up) - 1u;                   // piece of slot lane + 32 sl
+                const uint32_t s0 = up ? 32u * sl + 31 - __clz(up) : last;     // its first slot
+                if (lane_id + 32u * sl < T) {
+                    if (sl == 0) {
+                        has = test_slot(top - 1 - r, lane_id - s0, x, c_lo, c_end, c_out);
+                    } else {
+                        bfs::PM<MAXV> yb;
+                        uint32_t b_lo = 0, b_end = 0;
+                        bool b_out = false;
+                        const bool hb = test_slot(top - 1 - r, lane_id + 32u * sl - s0, yb, b_lo, b_end, b_out);
+                        if (hb) stage_put<MAXV>(sg + (sl - 1) * Stage<MAXV>::F * 32, lane_id, yb, b_lo, b_end, b_out);
+                        hmask |= hb ? 1u << sl : 0u;
+                    }
+                }
+                before += __popc(m[sl]);
+                if (m[sl]) last = 32u * sl + 31 - __clz(m[sl]);
+            }
             __syncwarp();
             // ---- pop the pieces taken whole; advance the split one (piece kf)
-            if (kf < top && kf < 64) {  // (kf = 64: the 64 examined pieces were all taken whole)
-                const uint32_t xk = (kf & 1) ? x1 : x0;
-                if ((kf >> 1) == lane_id && xk < T) {
+            if (kf < top && kf < 32u * kSlots && kf / kSlots == lane_id) {
+                uint32_t xk = xs[0];
+#pragma unroll
+                for (int i = 1; i < kSlots; i++)
+                    if (kf % kSlots == (uint32_t)i) xk = xs[i];
+                if (xk < T) {
                     stk[1 * CAP + top - 1 - kf] += T - xk;
                     stk[2 * CAP + top - 1 - kf] -= T - xk;
                 }
@@ -614,11 +649,11 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
         }
         // ---- the new partial matches' windows go on top of the stack (depth first): the first
         // slot's children (or the items) from registers, then the second slot's from staging
-        for (int half = 0; half < 2; half++) {
-            if (half == 1) {
-                if (!__any_sync(kFull, has_b)) break;
-                has = has_b;
-                if (has_b) stage_get<MAXV>(sgb, lane_id, x, c_lo, c_end, c_out, s_nodes);
+        for (int sl = 0; sl < kSlots; sl++) {
+            if (sl >= 1) {
+                has = (hmask >> sl) & 1u;
+                if (!__any_sync(kFull, has)) continue;
+                if (has) stage_get<MAXV>(sg + (sl - 1) * Stage<MAXV>::F * 32, lane_id, x, c_lo, c_end, c_out, s_nodes);
             }
             if (__any_sync(kFull, has))
                 open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, has, x, c_lo, c_end, c_out,

@@ -126,12 +126,29 @@ __device__ __forceinline__ uint32_t first_after(const uint32_t *off, const uint2
     return lo;
 }
 
-__global__ void k_succ(const uint32_t *src, const uint32_t *dst, const uint32_t *tr, const uint32_t *out_off,
-                       const uint2 *out_ent, const uint32_t *in_off, const uint2 *in_ent, uint32_t E, uint4 *eptr) {
+// Successor pointers P(e).  Components 0 (out(src)) and 1 (in(dst)): edge e sits
+// in those lists itself, at list position pos, so P is the first position after pos with a later
+// time rank -- a forward step over the (rare) ties, no search (k_succ_own, one thread per list
+// position).  Components 2 (out(dst)) and 3 (in(src)) need a search in another vertex's list
+// (k_succ_cross).  eptr as u32 words: P(e) component k at eptr[4e + k].
+__global__ void k_succ_own(const uint32_t *ids, const uint2 *ent, const uint32_t *tr, uint32_t N, uint32_t k,
+                           uint32_t *eptr) {
+    for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < N; pos += gridDim.x * blockDim.x) {
+        const uint32_t e = ids[pos];
+        if (e == 0xFFFFFFFFu) continue;  // a sentinel position
+        const uint32_t key = tr[e];
+        uint32_t q = pos + 1;
+        while (ent[q].x <= key) ++q;  // ties; the list's sentinel (time rank 0xFFFFFFFF) stops it
+        eptr[4 * (size_t)e + k] = q;
+    }
+}
+__global__ void k_succ_cross(const uint32_t *src, const uint32_t *dst, const uint32_t *tr, const uint32_t *out_off,
+                             const uint2 *out_ent, const uint32_t *in_off, const uint2 *in_ent, uint32_t E,
+                             uint32_t *eptr) {
     for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
         const uint32_t a = src[e], b = dst[e], key = tr[e];
-        eptr[e] = make_uint4(first_after(out_off, out_ent, a, key), first_after(in_off, in_ent, b, key),
-                             first_after(out_off, out_ent, b, key), first_after(in_off, in_ent, a, key));
+        eptr[4 * (size_t)e + 2] = first_after(out_off, out_ent, b, key);
+        eptr[4 * (size_t)e + 3] = first_after(in_off, in_ent, a, key);
     }
 }
 
@@ -441,10 +458,14 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     trace("load: out/in CSR");
     // 4. successor pointers, then each list entry's copy of them
     if (E) {
-        k_succ<<<blocks_for(E), kT, 0, s>>>(g->d_src, g->d_dst, g->d_tr, g->d_out_off,
-                                            reinterpret_cast<const uint2 *>(g->d_out_ent), g->d_in_off,
-                                            reinterpret_cast<const uint2 *>(g->d_in_ent), E,
-                                            reinterpret_cast<uint4 *>(g->d_eptr));
+        for (uint32_t dir = 0; dir < 2; dir++) {
+            k_succ_own<<<blocks_for(N), kT, 0, s>>>(ids[dir], reinterpret_cast<const uint2 *>(dir == 0 ? g->d_out_ent : g->d_in_ent),
+                                                    g->d_tr, (uint32_t)N, dir, g->d_eptr);
+            count_launch();
+        }
+        k_succ_cross<<<blocks_for(E), kT, 0, s>>>(g->d_src, g->d_dst, g->d_tr, g->d_out_off,
+                                                  reinterpret_cast<const uint2 *>(g->d_out_ent), g->d_in_off,
+                                                  reinterpret_cast<const uint2 *>(g->d_in_ent), E, g->d_eptr);
         count_launch();
     }
     if (N) {

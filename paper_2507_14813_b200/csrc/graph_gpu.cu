@@ -194,6 +194,16 @@ __global__ void k_proxy(const int64_t *t, uint32_t E, int64_t delta, const uint3
             const uint32_t *off = (k == 0 || k == 2) ? out_off : in_off;
             const uint2 *ent = (k == 0 || k == 2) ? out_ent : in_ent;
             uint32_t lo = st[k], hi = off[xs[k] + 1] - 1;
+            // first position in [lo, hi] with time rank > H: gallop from lo (windows are short),
+            // then bisect -- the same position the host's binary search finds
+            for (uint32_t step = 1; lo < hi; step <<= 1) {
+                const uint32_t probe = min(hi, lo + step - 1);
+                if (ent[probe].x > H) {
+                    hi = probe;
+                    break;
+                }
+                lo = probe + 1;
+            }
             while (lo < hi) {
                 const uint32_t m = lo + ((hi - lo) >> 1);
                 if (ent[m].x > H) hi = m;

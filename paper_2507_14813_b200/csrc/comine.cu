@@ -874,10 +874,6 @@ mayura_status mine(mayura_graph_s *g, const DeviceTable &dt, uint32_t r0, uint32
         wdfs::WParams w;
         w.b = bfs_params(g, dt, r0, n_roots, counts, stats, 0u);
         w.b.in.data = nullptr;
-        if (!st && !getenv("MAYURA_WINDOW_END_KERNEL")) {  // hi(root) computed at intake (run() skipped a2)
-            w.b.T = g->d_t;
-            w.b.delta = delta;
-        }
         w.gwant = dt.gwant;
         w.lb = lb;
         w.direct = 1;
@@ -998,13 +994,8 @@ mayura_status run(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint64_t r
     // the flat form computes hi in its level-0 pass and uses no scheduler words: only the
     // counts need zeroing (one memset instead of the window_end_kernel launch)
     const bool flat_only = kernel_kind(g) == K_FLAT && !stats_host && tabs[0].max_edges > 1;
-    // the warp form likewise computes hi(root) when it takes a root (no window_end_kernel): only the
-    // counts and its item cursors need zeroing
-    bool warp_fused = kernel_kind(g) == K_WARP && !stats_host && !getenv("MAYURA_WINDOW_END_KERNEL");
-    for (size_t i = 0; i < tabs.size() && warp_fused; i++) warp_fused = wdfs_fits(tabs[i]);
-    if (flat_only || warp_fused) CK(cudaMemsetAsync(d_counts, 0, sizeof(unsigned long long) * k, s), "cudaMemsetAsync(counts)");
-    if (warp_fused) CK(cudaMemsetAsync(g->d_queue, 0, sizeof(uint32_t) * n_lb, s), "cudaMemsetAsync(queue)");
-    if (!flat_only && !warp_fused) {
+    if (flat_only) CK(cudaMemsetAsync(d_counts, 0, sizeof(unsigned long long) * k, s), "cudaMemsetAsync(counts)");
+    if (!flat_only) {
         const int threads = 256;
         uint32_t blocks = (n_roots + threads - 1) / threads;
         const uint32_t minb = (std::max(n_lb, k) + threads - 1) / threads;

@@ -572,23 +572,9 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
             if (lane_id < take) {
                 if (w.direct) {  // a root edge: count the root node's completion, expand it if inner
                     const uint32_t r = p.r0 + item;
-                    const uint32_t rs = __ldg(p.src + r), rd = __ldg(p.dst + r);
-                    if (rs != rd) {  // a self-loop never matches canonical 0->1 (reading R7)
+                    if (bfs::load_root<MAXV>(p, r, x)) {
                         if (root.flags & NODE_COMPLETION) cnt_add(root.slot);
                         has = (root.flags & NODE_INNER) != 0;
-                        if (has) {
-#pragma unroll
-                            for (int k = 0; k < MAXV; k++) x.m2g[k] = kNone;
-                            x.m2g[0] = rs;
-                            x.m2g[1] = rd;
-                            x.node = 0;
-                            x.nv = 2;
-                            x.root = r;
-                            x.tr_prev = __ldg(p.tr + r);
-                            x.P = __ldg(p.eptr + r);
-                            // hi(root) (step a2) here, unless window_end_kernel ran before (p.T null)
-                            x.h = p.T ? window_end_of(p.T, p.E, p.delta, r) : __ldg(p.hi + r);
-                        }
                     }
                 } else if (item < n_pm) {  // a partial match of the breadth-first level (counted there)
                     bfs::load_rec<MAXV>(p, s_pref, item, x);

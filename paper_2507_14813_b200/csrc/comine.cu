@@ -345,7 +345,7 @@ cudaError_t launch_wdfs_t(const wdfs::WParams &w, size_t smem, cudaStream_t s, i
 template <int MAXV, int CAP>
 cudaError_t launch_wdfs_c(wdfs::WParams w, bool generic, bool stats, cudaStream_t s, int sms) {
     const bfs::BParams &b = w.b;
-    w.lanecnt = (size_t)b.n_slots * wdfs::kWB * 4 <= kLaneCntSmem ? 1u : 0u;
+    w.lanecnt = (size_t)b.n_slots * wdfs::kWB * sizeof(wdfs::cnt_t) <= kLaneCntSmem ? 1u : 0u;
     w.o_cnt = (uint32_t)wdfs::off_cnt(b.n_nodes, b.n_groups, b.n_slots);
     w.o_stk = (uint32_t)wdfs::off_stk(b.n_nodes, b.n_groups, b.n_slots, w.lanecnt != 0);
     const size_t smem = wdfs::smem_bytes(b.n_nodes, b.n_groups, b.n_slots, w.lanecnt != 0, MAXV, CAP);
@@ -410,7 +410,7 @@ mayura_status launch_wdfs(mayura_graph_s *g, wdfs::WParams w, uint32_t max_verti
 
 // the warp kernel's stacks fit the block's shared memory (else the lane kernel is used)
 bool wdfs_fits(const DeviceTable &dt) {
-    const bool lc = (size_t)dt.n_slots * wdfs::kWB * 4 <= kLaneCntSmem;
+    const bool lc = (size_t)dt.n_slots * wdfs::kWB * sizeof(wdfs::cnt_t) <= kLaneCntSmem;
     return wdfs::smem_bytes(dt.n_nodes, dt.n_groups, dt.n_slots, lc, (int)mv_class(dt.max_vertices), wdfs::kCap) <=
            200 * 1024;
 }

@@ -298,7 +298,7 @@ __device__ __forceinline__ void emit(const BParams &p, const lane::LNode *nodes,
         if (STATS) c.st[ST_BYTES] += 0;  // frontier traffic is not algorithmic
     } else {
         if (STATS) c.st[ST_CONTEXTS]++;
-        atomicAdd(p.fallback, 1u);
+        if (p.fallback) atomicAdd(p.fallback, 1u);
         dfs<MAXV, STATS>(p, nodes, groups, y, c);
     }
 }

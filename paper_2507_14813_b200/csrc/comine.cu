@@ -809,7 +809,9 @@ bfs::BParams bfs_params(const mayura_graph_s *g, const DeviceTable &dt, uint32_t
     b.n_nodes = dt.n_nodes; b.n_groups = dt.n_groups; b.n_motifs = dt.n_motifs; b.n_slots = dt.n_slots;
     b.r0 = r0; b.n_roots = n_roots;
     b.long_items = g->d_bfs_long; b.long_cap = g->bfs_long_cap;
-    b.fallback = g->d_bfs_ctl + kCtlWords * bfs::kMaxLevels;
+    // diagnostic counters in the control words; null when this graph has none allocated (the warp
+    // form allocates no breadth-first scratch): the kernels skip the count then
+    b.fallback = g->d_bfs_ctl ? g->d_bfs_ctl + kCtlWords * bfs::kMaxLevels : nullptr;
     b.inline_preleaf = inline_preleaf;
     b.heavy_min = 0;  // set by mine() for the hybrid's single breadth-first level
     b.T = nullptr;    // set by the flat path: its level-0 pass computes (and stores) hi itself
@@ -817,7 +819,7 @@ bfs::BParams bfs_params(const mayura_graph_s *g, const DeviceTable &dt, uint32_t
     b.E = (uint32_t)g->E;
     b.hi_w = g->d_hi;
     b.light = nullptr;
-    b.light_cnt = g->d_bfs_ctl + kCtlWords * bfs::kMaxLevels + 1;
+    b.light_cnt = g->d_bfs_ctl ? g->d_bfs_ctl + kCtlWords * bfs::kMaxLevels + 1 : nullptr;
     b.counts = counts; b.stats = stats;
     return b;
 }

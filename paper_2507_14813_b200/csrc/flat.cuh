@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kTB) flat_win_kernel(const __grid_constant__ F
                     }
                 } else {  // no room: empty the reserved slots that exist, mine the rest in place
                     for (uint32_t q = at; q < at + np && q < f.win_seg_cap; q++) wseg[(size_t)q * PW] = make_uint4(0, 0, 0, 0);
-                    atomicAdd(p.fallback, 1u);
+                    if (p.fallback) atomicAdd(p.fallback, 1u);
                     bfs::dfs<MAXV, false>(p, s.nodes, s.groups, x, c, g);
                     fell = true;
                 }

@@ -346,7 +346,7 @@ __device__ __forceinline__ void open_push(const WParams &w, const lane::LNode *s
 #pragma unroll
                 for (int k = 0; k < MAXV; k++) stk[(6 + k) * CAP + slot] = x.m2g[k];
             } else {
-                atomicAdd(p.fallback, 1u);
+                if (p.fallback) atomicAdd(p.fallback, 1u);
                 bfs::PM<MAXV> y = x;
                 if (c_end)  // a child: its successor pointers may not have been loaded with the entry
                     y.P = __ldg((c_out ? p.out_ptr : p.in_ptr) + (c_lo - 1));

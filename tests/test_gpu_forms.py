@@ -5,6 +5,8 @@ default for larger graphs), "warp" (the warp kernel straight from the roots), "l
 per-lane depth-first kernel) and "mixed".  Random groups, hub lists, the C1 workload, the
 87-motif 3-edge family (every anchor kind incl. GLOBAL), and forced overflow of the
 window-piece and frontier buffers (the depth-first fallback must keep counts exact)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -147,3 +149,22 @@ def test_form_many_single_entry_windows(M, oracle_mod):
         src, dst, t, V = synth.random_graph(400 + seed, 3000, 60_000, 200_000, 0.002)
         motifs = synth.group(synth.GROUP_C2) + [synth.MOTIFS["recip2"], synth.MOTIFS["path2"]]
         assert run(M, src, dst, t, V, motifs, 400) == oracle_mod.backtrack(src, dst, t, V, motifs, 400)
+
+
+def test_warp_form_fresh_process_fallback(oracle_mod):
+    """The warp form's serial fallback (full stack, no spill area) in a process that never ran
+    another form: its graph has no breadth-first scratch, so the kernel's diagnostic fallback
+    counter must not be dereferenced (it was, through a null control-word pointer, before r2)."""
+    import subprocess
+    import sys
+    code = (
+        "import os, sys; sys.path.insert(0, %r)\\n"
+        "os.environ.update(MAYURA_KERNEL='warp', MAYURA_WDFS_SMALL='1', MAYURA_WDFS_SPILL_CAP='0')\\n"
+        "import synth, oracle, paper_2507_14813_b200 as M\\n"
+        "src, dst, t, V = synth.random_graph(90, 6, 6000, 3000, 0.01)\\n"
+        "mo = synth.group(synth.GROUP_C4)\\n"
+        "g = M.Graph(src, dst, t, V, device=0); tree = M.MGTree(mo, 40)\\n"
+        "assert M.comine(g, tree) == oracle.backtrack(src, dst, t, V, mo, 40)\\n"
+        "print('ok')\\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]

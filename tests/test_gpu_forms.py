@@ -158,13 +158,13 @@ def test_warp_form_fresh_process_fallback(oracle_mod):
     import subprocess
     import sys
     code = (
-        "import os, sys; sys.path.insert(0, %r)\\n"
-        "os.environ.update(MAYURA_KERNEL='warp', MAYURA_WDFS_SMALL='1', MAYURA_WDFS_SPILL_CAP='0')\\n"
-        "import synth, oracle, paper_2507_14813_b200 as M\\n"
-        "src, dst, t, V = synth.random_graph(90, 6, 6000, 3000, 0.01)\\n"
-        "mo = synth.group(synth.GROUP_C4)\\n"
-        "g = M.Graph(src, dst, t, V, device=0); tree = M.MGTree(mo, 40)\\n"
-        "assert M.comine(g, tree) == oracle.backtrack(src, dst, t, V, mo, 40)\\n"
-        "print('ok')\\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        "import os, sys; sys.path.insert(0, %r)\n"
+        "os.environ.update(MAYURA_KERNEL='warp', MAYURA_WDFS_SMALL='1', MAYURA_WDFS_SPILL_CAP='0')\n"
+        "import synth, oracle, paper_2507_14813_b200 as M\n"
+        "src, dst, t, V = synth.random_graph(90, 6, 6000, 3000, 0.01)\n"
+        "mo = synth.group(synth.GROUP_C4)\n"
+        "g = M.Graph(src, dst, t, V, device=0); tree = M.MGTree(mo, 40)\n"
+        "assert M.comine(g, tree) == oracle.backtrack(src, dst, t, V, mo, 40)\n"
+        "print('ok')\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]

@@ -142,13 +142,17 @@ __global__ void k_succ_own(const uint32_t *ids, const uint2 *ent, const uint32_t
         eptr[4 * (size_t)e + k] = q;
     }
 }
-__global__ void k_succ_cross(const uint32_t *src, const uint32_t *dst, const uint32_t *tr, const uint32_t *out_off,
-                             const uint2 *out_ent, const uint32_t *in_off, const uint2 *in_ent, uint32_t E,
-                             uint32_t *eptr) {
-    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
-        const uint32_t a = src[e], b = dst[e], key = tr[e];
-        eptr[4 * (size_t)e + 2] = first_after(out_off, out_ent, b, key);
-        eptr[4 * (size_t)e + 3] = first_after(in_off, in_ent, a, key);
+// Components 2 (out(dst)) and 3 (in(src)), one thread per list position: the edges of in(b) are
+// consecutive positions, and all of them search out(b) (component 2) -- neighbouring threads search
+// the same list at nearby keys (cache-friendly, unlike one thread per edge id); likewise the edges
+// of out(a) search in(a) (component 3).  `other` = the list searched, `x_of` = dst (k = 2) or src
+// (k = 3) of the edge.
+__global__ void k_succ_cross(const uint32_t *ids, const uint32_t *x_of, const uint32_t *tr, const uint32_t *off,
+                             const uint2 *ent, uint32_t N, uint32_t k, uint32_t *eptr) {
+    for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < N; pos += gridDim.x * blockDim.x) {
+        const uint32_t e = ids[pos];
+        if (e == 0xFFFFFFFFu) continue;  // a sentinel position
+        eptr[4 * (size_t)e + k] = first_after(off, ent, x_of[e], tr[e]);
     }
 }
 
@@ -473,9 +477,14 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
                                                     g->d_tr, (uint32_t)N, dir, g->d_eptr);
             count_launch();
         }
-        k_succ_cross<<<blocks_for(E), kT, 0, s>>>(g->d_src, g->d_dst, g->d_tr, g->d_out_off,
-                                                  reinterpret_cast<const uint2 *>(g->d_out_ent), g->d_in_off,
-                                                  reinterpret_cast<const uint2 *>(g->d_in_ent), E, g->d_eptr);
+        // component 2 = out(dst) over the in-list positions, component 3 = in(src) over the out-list ones
+        k_succ_cross<<<blocks_for(N), kT, 0, s>>>(ids[1], g->d_dst, g->d_tr, g->d_out_off,
+                                                  reinterpret_cast<const uint2 *>(g->d_out_ent), (uint32_t)N, 2u,
+                                                  g->d_eptr);
+        count_launch();
+        k_succ_cross<<<blocks_for(N), kT, 0, s>>>(ids[0], g->d_src, g->d_tr, g->d_in_off,
+                                                  reinterpret_cast<const uint2 *>(g->d_in_ent), (uint32_t)N, 3u,
+                                                  g->d_eptr);
         count_launch();
     }
     if (N) {

@@ -168,3 +168,19 @@ def test_warp_form_fresh_process_fallback(oracle_mod):
         "print('ok')\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_warp_stats_instance(oracle_mod, monkeypatch):
+    """MAYURA_WDFS_STATS=1: the instrumented warp kernel (tools/wdfs_stats.py) counts exactly the
+    oracle's matches; every round gives at most 64 candidates and every valid entry is a lane."""
+    import paper_2507_14813_b200 as M
+    monkeypatch.setenv("MAYURA_KERNEL", "warp")
+    monkeypatch.setenv("MAYURA_WDFS_STATS", "1")
+    src, dst, t, V = synth.random_graph(77, 40, 5000, 2000, 0.01)
+    motifs = synth.group(synth.GROUP_C2)
+    g = M.Graph(src, dst, t, V, device=0)
+    tree = M.MGTree(motifs, 60)
+    st = M.comine_stats(g, tree)
+    exp = oracle_mod.backtrack(src, dst, t, V, motifs, 60)
+    assert st["matches"] == sum(exp) and M.comine(g, tree) == exp
+    assert st["batches"] > 0 and st["probes"] <= 64 * st["batches"] and st["entries"] <= st["probes"]

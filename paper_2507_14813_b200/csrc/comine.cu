@@ -20,6 +20,7 @@
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX ranges (visible under nsys / ncu --nvtx)
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>

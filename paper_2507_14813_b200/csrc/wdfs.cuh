@@ -101,7 +101,7 @@ __host__ __device__ inline size_t off_info(uint32_t nn, uint32_t ng, uint32_t ns
            lane::align16((size_t)ns * 8);
 }
 __host__ __device__ inline size_t off_cnt(uint32_t nn, uint32_t ng, uint32_t ns) {
-    return off_info(nn, ng, ns) + lane::align16((size_t)nn * 4) + 2 * lane::align16((size_t)ng * 4);
+    return off_info(nn, ng, ns) + lane::align16((size_t)nn * 4) + 3 * lane::align16((size_t)ng * 4);
 }
 __host__ __device__ inline size_t off_stk(uint32_t nn, uint32_t ng, uint32_t ns, bool lanecnt) {
     return lane::align16(off_cnt(nn, ng, ns) + (lanecnt ? (size_t)ns * kWB * sizeof(cnt_t) : 0));
@@ -250,6 +250,19 @@ __device__ __forceinline__ uint32_t node_info(const lane::LNode &n) {
            ((n.flags & NODE_INNER) ? NI_INNER : 0u) | ((uint32_t)(n.n_new & 3u) << 18) | ((uint32_t)n.nv << 24);
 }
 
+// Per group, the shape of the star chains' last level: exactly one child, a leaf (a completion
+// with no children) that wants a NEW vertex from an OUT/IN list.  GL_FLAG | mapped vertices of the
+// parent << 16 | the child's completion slot; 0 otherwise.  A round whose candidates all belong to
+// such a group runs the specialised leaf_round<NV> (NV compile-time: the m2g compares unrolled to
+// exactly the mapped vertices, the slot an operand, no child lookup).
+constexpr uint32_t GL_FLAG = 1u << 31;
+__device__ __forceinline__ uint32_t group_leaf(const DGroup &G, const lane::LNode *nodes) {
+    if (G.kind == ANCHOR_GLOBAL || G.child_end - G.child_begin != 1) return 0u;
+    const lane::LNode c = nodes[G.child_begin];
+    if ((c.flags & NODE_INNER) || !(c.flags & NODE_COMPLETION) || c.want != CLS_NEW || c.n_new != 1) return 0u;
+    return GL_FLAG | ((uint32_t)(c.nv - 1) << 16) | (uint32_t)(c.slot & 0xFFFFu);
+}
+
 // Per-warp staging area (shared memory, SoA, 32 slots = one per lane) of the children found by a
 // round's second slots, expanded after the first slots' ones.  Words: 0 node | c_out << 31,
 // 1 tr_prev, 2 h, 3 root, 4..7 P, 8 c_lo, 9 c_end, 10.. m2g[MAXV]
@@ -387,11 +400,13 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
     uint32_t *s_ninfo = reinterpret_cast<uint32_t *>(smem + off_info(p.n_nodes, p.n_groups, p.n_slots));
     uint32_t *s_ginfo = s_ninfo + lane::align16((size_t)p.n_nodes * 4) / 4;
     uint32_t *s_gw = s_ginfo + lane::align16((size_t)p.n_groups * 4) / 4;
+    uint32_t *s_gleaf = s_gw + lane::align16((size_t)p.n_groups * 4) / 4;
     for (uint32_t i = tid; i < p.n_nodes; i += kWB) s_nodes[i] = p.nodes[i];
     for (uint32_t i = tid; i < p.n_groups; i += kWB) s_groups[i] = p.groups[i];
     for (uint32_t i = tid; i < p.n_groups; i += kWB) s_gw[i] = w.gwant[i];
     for (uint32_t g = tid; g < p.n_groups; g += kWB) s_ginfo[g] = group_info(p.groups[g], p.nodes);
     for (uint32_t n = tid; n < p.n_nodes; n += kWB) s_ninfo[n] = node_info(p.nodes[n]);
+    for (uint32_t g = tid; g < p.n_groups; g += kWB) s_gleaf[g] = group_leaf(p.groups[g], p.nodes);
     for (uint32_t i = tid; i < p.n_slots; i += kWB) s_tot[i] = 0;
     if (s_cnt)
         for (uint32_t i = 0; i < p.n_slots; i++) s_cnt[i * kWB + tid] = 0;
@@ -434,6 +449,29 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
     uint32_t sp_top = 0;       // warp-uniform spilled pieces (global memory)
     uint32_t cb = 0, cl = 0;   // warp-uniform item chunk
     bool items_left = true;
+
+    // The specialised round of a leaf group (all candidates in one group whose only child is a leaf
+    // wanting a NEW vertex, with NV mapped vertices before it): per slot, the entry, the time test
+    // and NV compares against the piece's mapped vertices; the completion slot is an operand.
+    auto leaf_round = [&](auto nv_tag, const uint32_t (&spi)[kSlots], const uint32_t (&sat)[kSlots], uint32_t T,
+                          uint32_t gl) {
+        constexpr int NV = decltype(nv_tag)::value;
+        const uint32_t slot = gl & 0xFFFFu;
+        const bool out = (s_ginfo[stk[0 * CAP + spi[0]]] & GI_KIND) == ANCHOR_OUT;
+        const uint2 *ent = out ? p.out_ent : p.in_ent;
+#pragma unroll
+        for (int sl = 0; sl < kSlots; sl++) {
+            if (lane_id + 32u * sl < T) {
+                const uint32_t pi = spi[sl];
+                const uint2 e = __ldg(ent + stk[1 * CAP + pi] + sat[sl]);
+                const uint32_t tp = stk[3 * CAP + pi], h = stk[4 * CAP + pi];
+                bool fresh = e.x > tp && e.x <= h;
+#pragma unroll
+                for (int k = 0; k < NV; k++) fresh = fresh && stk[(6 + k) * CAP + pi] != e.y;
+                if (fresh) cnt_add(slot);
+            }
+        }
+    };
 
     // Test the candidate entry of one slot: window entry `at` of piece `pi`.  Completions are
     // counted; an inner hit fills y (the child partial match) and its continuation window.
@@ -620,25 +658,46 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
                 st[ST_BATCHES]++;
                 st[ST_PROBES] += T;
             }
+            uint32_t spi[kSlots], sat[kSlots];
+            bool same = true;  // every candidate of the round is in the top piece's group
+            const uint32_t g0 = stk[0 * CAP + top - 1];
 #pragma unroll
             for (int sl = 0; sl < kSlots; sl++) {
                 const uint32_t up = m[sl] & le;
                 const uint32_t r = before + __popc(up) - 1u;                   // piece of slot lane + 32 sl
                 const uint32_t s0 = up ? 32u * sl + 31 - __clz(up) : last;     // its first slot
-                if (lane_id + 32u * sl < T) {
-                    if (sl == 0) {
-                        has = test_slot(top - 1 - r, lane_id - s0, x, c_lo, c_end, c_out);
-                    } else {
-                        bfs::PM<MAXV> yb;
-                        uint32_t b_lo = 0, b_end = 0;
-                        bool b_out = false;
-                        const bool hb = test_slot(top - 1 - r, lane_id + 32u * sl - s0, yb, b_lo, b_end, b_out);
-                        if (hb) stage_put<MAXV>(sg + (sl - 1) * Stage<MAXV>::F * 32, lane_id, yb, b_lo, b_end, b_out);
-                        hmask |= hb ? 1u << sl : 0u;
-                    }
-                }
+                spi[sl] = top - 1 - r;
+                sat[sl] = lane_id + 32u * sl - s0;
+                if (lane_id + 32u * sl < T) same = same && stk[0 * CAP + spi[sl]] == g0;
                 before += __popc(m[sl]);
                 if (m[sl]) last = 32u * sl + 31 - __clz(m[sl]);
+            }
+            const uint32_t gl = s_gleaf[g0];
+            if (!STATS && gl && __all_sync(kFull, same)) {
+                // a leaf round: the group's single child is a leaf wanting a NEW vertex
+                const uint32_t nvp = (gl >> 16) & 0xFFu;
+                if (nvp <= 2) leaf_round(std::integral_constant<int, 2>{}, spi, sat, T, gl);
+                else if (nvp == 3 || MAXV <= 3) leaf_round(std::integral_constant<int, (MAXV < 3 ? MAXV : 3)>{}, spi, sat, T, gl);
+                else if (nvp == 4 || MAXV <= 4) leaf_round(std::integral_constant<int, (MAXV < 4 ? MAXV : 4)>{}, spi, sat, T, gl);
+                else if (nvp == 5 || MAXV <= 5) leaf_round(std::integral_constant<int, (MAXV < 5 ? MAXV : 5)>{}, spi, sat, T, gl);
+                else if (nvp == 6 || MAXV <= 6) leaf_round(std::integral_constant<int, (MAXV < 6 ? MAXV : 6)>{}, spi, sat, T, gl);
+                else leaf_round(std::integral_constant<int, MAXV>{}, spi, sat, T, gl);
+            } else {
+#pragma unroll
+                for (int sl = 0; sl < kSlots; sl++) {
+                    if (lane_id + 32u * sl < T) {
+                        if (sl == 0) {
+                            has = test_slot(spi[sl], sat[sl], x, c_lo, c_end, c_out);
+                        } else {
+                            bfs::PM<MAXV> yb;
+                            uint32_t b_lo = 0, b_end = 0;
+                            bool b_out = false;
+                            const bool hb = test_slot(spi[sl], sat[sl], yb, b_lo, b_end, b_out);
+                            if (hb) stage_put<MAXV>(sg + (sl - 1) * Stage<MAXV>::F * 32, lane_id, yb, b_lo, b_end, b_out);
+                            hmask |= hb ? 1u << sl : 0u;
+                        }
+                    }
+                }
             }
             __syncwarp();
             // ---- pop the pieces taken whole; advance the split one (piece kf)

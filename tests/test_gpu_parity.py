@@ -13,6 +13,7 @@ import pytest
 
 import synth
 from tests import _pins
+from tests._sample import oracle_on_time_windows
 
 pytestmark = pytest.mark.gpu
 
@@ -324,7 +325,7 @@ def test_config_c5_sampled_parity_full_size(M, oracle_mod):
     E = g.n_edges
     full = M.comine(g, tree)
     ranges = [(i * (E // 4) + E // 8, i * (E // 4) + E // 8 + 2000) for i in range(4)]
-    per, _, _ = oracle_mod.backtrack_ranges(src, dst, t, V, cfg.group(), cfg.delta, ranges)
+    per = oracle_on_time_windows(oracle_mod, src, dst, t, V, cfg.group(), cfg.delta, ranges)
     for rg, exp in zip(ranges, per):
         assert M.comine(g, tree, rg) == exp, rg
     # planted patterns: every planted instance is a match (lower bounds; the background adds more)

@@ -11,6 +11,7 @@ import pytest
 
 import synth
 from tests import _pins
+from tests._sample import oracle_on_time_windows
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "hand_examples.json")
 
@@ -294,3 +295,13 @@ def test_backtrack_ranges_equals_single_ranges(oracle_mod):
     per, build_s, mine_s = oracle_mod.backtrack_ranges(src, dst, t, V, motifs, 20, ranges, threads=3)
     assert per == [oracle_mod.backtrack(src, dst, t, V, motifs, 20, root_range=r) for r in ranges]
     assert build_s >= 0 and mine_s >= 0
+
+
+def test_time_window_subgraph_oracle(oracle_mod):
+    """The time-window reduction used by the full-size C5 test equals the oracle on the whole graph
+    (tie-heavy random graph, ranges starting inside tie groups)."""
+    src, dst, t, V = synth.random_graph(4242, 30, 3000, 400)
+    motifs = synth.group(synth.GROUP_C2)
+    ranges = [(0, 50), (700, 913), (1500, 1501), (2950, 3000)]
+    assert oracle_on_time_windows(oracle_mod, src, dst, t, V, motifs, 25, ranges) == \
+        [oracle_mod.backtrack(src, dst, t, V, motifs, 25, root_range=r) for r in ranges]

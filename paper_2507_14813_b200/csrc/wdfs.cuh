@@ -53,6 +53,10 @@ constexpr int kWarps = kWB / 32;
 #define WDFS_CAP 96  // r2 sweep on C4: 64 / 80 / 96 / 128 -> 78.1 / 77.3 / 75.4 / 77.8 ms
 #endif
 constexpr int kCap = WDFS_CAP;           // pieces per warp stack in shared memory
+#ifndef WDFS_PRE
+#define WDFS_PRE 2  // anchor groups of a new partial match whose windows are located together (2: C4 -4 %, 3 spills)
+#endif
+constexpr int kPre = WDFS_PRE;
 constexpr int kCapSmall = 64;            // test instance (MAYURA_WDFS_SMALL=1): spills early and often
 constexpr uint8_t NODE_NEEDP = 16;       // LNode flag: a group of the node needs its edge's successor
                                          // pointers (a START_P* group that is not a same-list continuation)
@@ -325,15 +329,38 @@ __device__ __forceinline__ void open_push(const WParams &w, const lane::LNode *s
         same = c_end ? xn.same : 0u;
     }
     const uint32_t mg = __reduce_max_sync(kFull, ng);
+    // the windows of the first kPre groups are located together (independent loads in flight at
+    // once), before any is pushed
+    uint32_t plo[kPre], pn[kPre];
+#pragma unroll
+    for (int q = 0; q < kPre; q++) {
+        plo[q] = 0;
+        pn[q] = 0;
+        if ((uint32_t)q < ng) {
+            if ((same >> q) & 1u) {
+                plo[q] = c_lo;
+                pn[q] = c_end > c_lo ? c_end - c_lo : 0u;
+                WCHECK(c_lo <= c_end + 1, "continuation c_lo %u c_end %u node %u", c_lo, c_end, x.node);
+            } else {
+                plo[q] = window<MAXV, GEN>(p, s_groups[gb + q], x, pn[q]);
+            }
+        }
+    }
     bool fell = false;
     for (uint32_t q = 0; q < mg; q++) {
         uint32_t lo = 0, n = 0;
         const bool mine = q < ng && !fell;
-        if (mine) {
+        if (q < (uint32_t)kPre) {
+#pragma unroll
+            for (int k = 0; k < kPre; k++)
+                if ((uint32_t)k == q) {
+                    lo = plo[k];
+                    n = pn[k];
+                }
+        } else if (mine) {
             if ((same >> q) & 1u) {
                 lo = c_lo;
                 n = c_end > c_lo ? c_end - c_lo : 0u;
-                WCHECK(c_lo <= c_end + 1, "continuation c_lo %u c_end %u node %u", c_lo, c_end, x.node);
             } else {
                 lo = window<MAXV, GEN>(p, s_groups[gb + q], x, n);
             }

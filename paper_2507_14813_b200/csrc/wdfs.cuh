@@ -53,8 +53,11 @@ constexpr int kWarps = kWB / 32;
 #define WDFS_CAP 96  // r2 sweep on C4: 64 / 80 / 96 / 128 -> 78.1 / 77.3 / 75.4 / 77.8 ms
 #endif
 constexpr int kCap = WDFS_CAP;           // pieces per warp stack in shared memory
+#ifndef WDFS_PROBE8
+#define WDFS_PROBE8 1  // window lengths from 8 consecutive loads (0: 4 probes + bisection; C4 -3 %, C3 -5 %)
+#endif
 #ifndef WDFS_PRE
-#define WDFS_PRE 2  // anchor groups of a new partial match whose windows are located together (2: C4 -4 %, 3 spills)
+#define WDFS_PRE 1  // anchor groups of a new partial match whose windows are located together (with PROBE8: 1 beats 2 by 0.7 %, 3 spills; w47)
 #endif
 constexpr int kPre = WDFS_PRE;
 constexpr int kCapSmall = 64;            // test instance (MAYURA_WDFS_SMALL=1): spills early and often
@@ -125,6 +128,20 @@ __device__ __forceinline__ bool in_window(const uint2 *ent, uint32_t lo, uint32_
     return lo + o < sent && __ldg(&ent[lo + o].x) <= h;
 }
 __device__ __forceinline__ uint32_t window_len(const uint2 *ent, uint32_t lo, uint32_t sent, uint32_t h) {
+#if WDFS_PROBE8
+    // every entry of the first 8 (two sectors): exact for windows of <= 7 entries, no dependent load
+    uint32_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) v[k] = __ldg(&ent[lo + k].x);
+    uint32_t b = kNone;
+#pragma unroll
+    for (int k = 7; k >= 0; k--)
+        if (lo + k >= sent || v[k] > h) b = k;
+    if (b != kNone) return b;
+    uint32_t a = 7;
+    b = 15;
+    {
+#else
     const uint32_t o[4] = {0, 1, 3, 7};
     uint32_t v[4];
 #pragma unroll
@@ -137,6 +154,7 @@ __device__ __forceinline__ uint32_t window_len(const uint2 *ent, uint32_t lo, ui
     if (b != kNone) {
         a = b == 1 ? 0 : (b - 1) / 2;  // the previous probe offset (in)
     } else {  // >= 8 entries: gallop
+#endif
         a = 7;
         b = 15;
         for (;;) {

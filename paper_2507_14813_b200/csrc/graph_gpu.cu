@@ -52,9 +52,15 @@ int bits_for(uint64_t maxval) {
     return b;
 }
 
-__global__ void k_check_ids(const uint32_t *src, const uint32_t *dst, uint32_t E, uint32_t V, uint32_t *bad) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x)
-        if (src[i] >= V || dst[i] >= V) atomicOr(bad, 1u);
+// vertex ids checked against V and packed (src | dst << 32), so the gather after the time sort
+// reads one 8-byte word per edge instead of two scattered 4-byte ones
+__global__ void k_check_pack(const uint32_t *src, const uint32_t *dst, uint32_t E, uint32_t V, uint32_t *bad,
+                             uint64_t *sd) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
+        const uint32_t a = src[i], b = dst[i];
+        if (a >= V || b >= V) atomicOr(bad, 1u);
+        sd[i] = (uint64_t)a | ((uint64_t)b << 32);
+    }
 }
 
 __global__ void k_iota_key(const int64_t *t, int64_t tmin, uint64_t *key, uint32_t *val, uint32_t E) {
@@ -64,27 +70,35 @@ __global__ void k_iota_key(const int64_t *t, int64_t tmin, uint64_t *key, uint32
     }
 }
 
-__global__ void k_gather(const uint32_t *perm, const uint32_t *isrc, const uint32_t *idst, const int64_t *it,
-                         uint32_t *src, uint32_t *dst, int64_t *t, uint32_t E) {
+// edge i of the time order: endpoints gathered from the packed input, the timestamp from the
+// sorted key itself (t - tmin, coalesced)
+__global__ void k_gather(const uint32_t *perm, const uint64_t *sd, const uint64_t *skey, int64_t tmin, uint32_t *src,
+                         uint32_t *dst, int64_t *t, uint32_t E) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
-        const uint32_t r = perm[i];
-        src[i] = isrc[r];
-        dst[i] = idst[r];
-        t[i] = it[r];
+        const uint64_t w = sd[perm[i]];
+        src[i] = (uint32_t)w;
+        dst[i] = (uint32_t)(w >> 32);
+        t[i] = (int64_t)(skey[i] + (uint64_t)tmin);
     }
 }
 
-// tr[i] = first index with t == t[i] (t sorted)
+// tr[i] = first index with t == t[i] (t sorted): a backward step over the (rare) ties, a
+// bisection when the tie run is long
 __global__ void k_time_rank(const int64_t *t, uint32_t *tr, uint32_t E) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
         const int64_t x = t[i];
-        uint32_t lo = 0, hi = i;
-        while (lo < hi) {
-            const uint32_t m = lo + ((hi - lo) >> 1);
-            if (t[m] < x) lo = m + 1;
-            else hi = m;
+        uint32_t j = i;
+        for (int s = 0; s < 8 && j > 0 && t[j - 1] == x; s++) j--;
+        if (j > 0 && t[j - 1] == x) {
+            uint32_t lo = 0, hi = j;
+            while (lo < hi) {
+                const uint32_t m = lo + ((hi - lo) >> 1);
+                if (t[m] < x) lo = m + 1;
+                else hi = m;
+            }
+            j = lo;
         }
-        tr[i] = lo;
+        tr[i] = j;
     }
 }
 
@@ -126,33 +140,25 @@ __device__ __forceinline__ uint32_t first_after(const uint32_t *off, const uint2
     return lo;
 }
 
-// Successor pointers P(e).  Components 0 (out(src)) and 1 (in(dst)): edge e sits
-// in those lists itself, at list position pos, so P is the first position after pos with a later
-// time rank -- a forward step over the (rare) ties, no search (k_succ_own, one thread per list
-// position).  Components 2 (out(dst)) and 3 (in(src)) need a search in another vertex's list
-// (k_succ_cross).  eptr as u32 words: P(e) component k at eptr[4e + k].
-__global__ void k_succ_own(const uint32_t *ids, const uint2 *ent, const uint32_t *tr, uint32_t N, uint32_t k,
-                           uint32_t *eptr) {
+// Successor pointers P(e), one thread per position of one direction's lists,
+// both components that position owns: the list's own component (0 = out(src) over the out-list
+// positions, 1 = in(dst) over the in-list ones) is the first position after pos with a later time
+// rank -- a forward step over the (rare) ties, no search; the cross component (3 = in(src) over the
+// out-list positions, 2 = out(dst) over the in-list ones) searches the owner's list of the other
+// direction -- neighbouring threads search the same list at nearby keys (cache-friendly, unlike one
+// thread per edge id).  The entry's time rank is its own list word (no gather of tr[e]); the two
+// words written land in one 16-byte eptr row.  eptr as u32 words: P(e) component k at eptr[4e + k].
+__global__ void k_succ(const uint32_t *ids, const uint2 *ent, const uint32_t *owner_of, const uint32_t *xoff,
+                       const uint2 *xent, uint32_t N, uint32_t k_own, uint32_t k_cross, uint32_t *eptr) {
     for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < N; pos += gridDim.x * blockDim.x) {
         const uint32_t e = ids[pos];
         if (e == 0xFFFFFFFFu) continue;  // a sentinel position
-        const uint32_t key = tr[e];
+        const uint32_t key = ent[pos].x;
+        const uint32_t x = owner_of[e];
         uint32_t q = pos + 1;
         while (ent[q].x <= key) ++q;  // ties; the list's sentinel (time rank 0xFFFFFFFF) stops it
-        eptr[4 * (size_t)e + k] = q;
-    }
-}
-// Components 2 (out(dst)) and 3 (in(src)), one thread per list position: the edges of in(b) are
-// consecutive positions, and all of them search out(b) (component 2) -- neighbouring threads search
-// the same list at nearby keys (cache-friendly, unlike one thread per edge id); likewise the edges
-// of out(a) search in(a) (component 3).  `other` = the list searched, `x_of` = dst (k = 2) or src
-// (k = 3) of the edge.
-__global__ void k_succ_cross(const uint32_t *ids, const uint32_t *x_of, const uint32_t *tr, const uint32_t *off,
-                             const uint2 *ent, uint32_t N, uint32_t k, uint32_t *eptr) {
-    for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < N; pos += gridDim.x * blockDim.x) {
-        const uint32_t e = ids[pos];
-        if (e == 0xFFFFFFFFu) continue;  // a sentinel position
-        eptr[4 * (size_t)e + k] = first_after(off, ent, x_of[e], tr[e]);
+        eptr[4 * (size_t)e + k_own] = q;
+        eptr[4 * (size_t)e + k_cross] = first_after(xoff, xent, x, key);
     }
 }
 
@@ -384,6 +390,8 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     GK(tmp.get(idst, E), "cudaMalloc(tmp)");
     GK(tmp.get(it, E), "cudaMalloc(tmp)");
     GK(tmp.get(bad, 4), "cudaMalloc(tmp)");
+    uint64_t *sd;
+    GK(tmp.get(sd, E), "cudaMalloc(tmp)");
     trace("load: allocations");
     // src/dst travel on a side stream while t is copied, reduced and sorted on the main one:
     // the sort by time needs only t, so the second half of the H2D traffic overlaps it
@@ -395,7 +403,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     GK(cudaMemcpyAsync(isrc, hsrc, 4ull * E, cudaMemcpyHostToDevice, ss.s2), "H2D(src)");
     GK(cudaMemcpyAsync(idst, hdst, 4ull * E, cudaMemcpyHostToDevice, ss.s2), "H2D(dst)");
     if (E) {
-        k_check_ids<<<blocks_for(E), kT, 0, ss.s2>>>(isrc, idst, E, V, bad);
+        k_check_pack<<<blocks_for(E), kT, 0, ss.s2>>>(isrc, idst, E, V, bad, sd);
         count_launch();
     }
     GK(cudaMemcpyAsync(ss.hbad, bad, 4, cudaMemcpyDeviceToHost, ss.s2), "D2H(check)");
@@ -437,11 +445,13 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
         char *ct;
         GK(tmp.get(ct, need), "cudaMalloc(tmp)");
         GK(cub::DeviceRadixSort::SortPairs(ct, need, key, key2, val, g->d_perm, (int)E, 0, tbits, s), "cub sort");
+        trace("load: time sort");
         // src/dst on the device and checked (host waits for the side stream only: the sort runs on)
         GK(cudaEventSynchronize(ss.ev2), "event sync");
         if (*ss.hbad) return fail(MAYURA_E_INVALID, "mayura_load_graph: vertex id >= n_vertices");
         GK(cudaStreamWaitEvent(s, ss.ev2, 0), "stream wait");
-        k_gather<<<blocks_for(E), kT, 0, s>>>(g->d_perm, isrc, idst, it, g->d_src, g->d_dst, g->d_t, E); count_launch();
+        k_gather<<<blocks_for(E), kT, 0, s>>>(g->d_perm, sd, key2, tmin, g->d_src, g->d_dst, g->d_t, E); count_launch();
+        trace("load: gather");
         // 2. time ranks
         k_time_rank<<<blocks_for(E), kT, 0, s>>>(g->d_t, g->d_tr, E); count_launch();
     }
@@ -465,6 +475,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
             char *ct;
             GK(tmp.get(ct, need), "cudaMalloc(tmp)");
             GK(cub::DeviceRadixSort::SortPairs(ct, need, k_in, skey, val, val2, (int)E, 0, vbits, s), "cub sort");
+            trace("load: vertex sort");
             k_scatter<<<blocks_for(E), kT, 0, s>>>(skey, val2, g->d_tr, nbr, E, ent, ids[dir]); count_launch();
         }
         k_offsets<<<blocks_for((uint64_t)V + 1), kT, 0, s>>>(skey, E, V, off); count_launch();
@@ -472,20 +483,14 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     trace("load: out/in CSR");
     // 4. successor pointers, then each list entry's copy of them
     if (E) {
-        for (uint32_t dir = 0; dir < 2; dir++) {
-            k_succ_own<<<blocks_for(N), kT, 0, s>>>(ids[dir], reinterpret_cast<const uint2 *>(dir == 0 ? g->d_out_ent : g->d_in_ent),
-                                                    g->d_tr, (uint32_t)N, dir, g->d_eptr);
-            count_launch();
-        }
-        // component 2 = out(dst) over the in-list positions, component 3 = in(src) over the out-list ones
-        k_succ_cross<<<blocks_for(N), kT, 0, s>>>(ids[1], g->d_dst, g->d_tr, g->d_out_off,
-                                                  reinterpret_cast<const uint2 *>(g->d_out_ent), (uint32_t)N, 2u,
-                                                  g->d_eptr);
+        // out-list positions: components 0 (own) and 3 (in(src)); in-list positions: 1 (own), 2 (out(dst))
+        k_succ<<<blocks_for(N), kT, 0, s>>>(ids[0], reinterpret_cast<const uint2 *>(g->d_out_ent), g->d_src, g->d_in_off,
+                                            reinterpret_cast<const uint2 *>(g->d_in_ent), (uint32_t)N, 0u, 3u, g->d_eptr);
         count_launch();
-        k_succ_cross<<<blocks_for(N), kT, 0, s>>>(ids[0], g->d_src, g->d_tr, g->d_in_off,
-                                                  reinterpret_cast<const uint2 *>(g->d_in_ent), (uint32_t)N, 3u,
-                                                  g->d_eptr);
+        k_succ<<<blocks_for(N), kT, 0, s>>>(ids[1], reinterpret_cast<const uint2 *>(g->d_in_ent), g->d_dst, g->d_out_off,
+                                            reinterpret_cast<const uint2 *>(g->d_out_ent), (uint32_t)N, 1u, 2u, g->d_eptr);
         count_launch();
+        trace("load: successor pointers (by edge)");
     }
     if (N) {
         k_entry_ptr<<<blocks_for(N), kT, 0, s>>>(ids[0], reinterpret_cast<const uint4 *>(g->d_eptr), g->d_perm,
@@ -497,7 +502,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     }
     GK(cudaGetLastError(), "graph build kernels");
     GK(cudaStreamSynchronize(s), "graph build");
-    trace("load: successor pointers");
+    trace("load: entry copies");
     return MAYURA_OK;
 }
 

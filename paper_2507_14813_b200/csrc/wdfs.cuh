@@ -600,12 +600,13 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
         // ---- the top 32 * kSlots pieces: candidate counts and their running sum (top first); lane l
         // holds pieces kSlots * l + i (one prefix sum of the per-lane sums)
         const uint32_t top = ps;
-        uint32_t pn[kSlots], incl[kSlots];
+        uint32_t pn[kSlots], incl[kSlots], pg[kSlots];
         uint32_t lsum = 0;
 #pragma unroll
         for (int i = 0; i < kSlots; i++) {
             const uint32_t idx = kSlots * lane_id + i;
             pn[i] = idx < top ? stk[2 * CAP + top - 1 - idx] : 0u;
+            pg[i] = idx < top ? stk[0 * CAP + top - 1 - idx] : 0u;  // its group (the leaf-round test)
             lsum += pn[i];
         }
         uint32_t linc = lsum;
@@ -681,16 +682,23 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
             // top pieces (the last one possibly split)
             const uint32_t T = min(tot, 32u * kSlots);
             uint32_t xs[kSlots], m[kSlots], kf = 0;
+            bool same = true;  // every candidate of the round is in the top piece's group
+            const uint32_t g0 = __shfl_sync(kFull, pg[0], 0);
+            {
+                uint32_t c[kSlots];
 #pragma unroll
-            for (int wv = 0; wv < kSlots; wv++) {
-                uint32_t c = 0;
+                for (int wv = 0; wv < kSlots; wv++) c[wv] = 0;
 #pragma unroll
                 for (int i = 0; i < kSlots; i++) {
-                    xs[i] = incl[i] - pn[i];  // first slot of piece kSlots * l + i
+                    xs[i] = incl[i] - pn[i];  // first slot of piece kSlots * l + i (pn = 0 past the top)
                     const bool pc = kSlots * lane_id + i < top && xs[i] < T;
-                    if (pc && (xs[i] >> 5) == (uint32_t)wv) c |= 1u << (xs[i] & 31);
+                    const uint32_t bit = pc ? 1u << (xs[i] & 31) : 0u;
+#pragma unroll
+                    for (int wv = 0; wv < kSlots; wv++) c[wv] |= (xs[i] >> 5) == (uint32_t)wv ? bit : 0u;
+                    same = same && (!pc || pg[i] == g0);
                 }
-                m[wv] = __reduce_or_sync(kFull, c);
+#pragma unroll
+                for (int wv = 0; wv < kSlots; wv++) m[wv] = __reduce_or_sync(kFull, c[wv]);
             }
 #pragma unroll
             for (int i = 0; i < kSlots; i++)
@@ -704,8 +712,6 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
                 st[ST_PROBES] += T;
             }
             uint32_t spi[kSlots], sat[kSlots];
-            bool same = true;  // every candidate of the round is in the top piece's group
-            const uint32_t g0 = stk[0 * CAP + top - 1];
 #pragma unroll
             for (int sl = 0; sl < kSlots; sl++) {
                 const uint32_t up = m[sl] & le;
@@ -713,7 +719,6 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
                 const uint32_t s0 = up ? 32u * sl + 31 - __clz(up) : last;     // its first slot
                 spi[sl] = top - 1 - r;
                 sat[sl] = lane_id + 32u * sl - s0;
-                if (lane_id + 32u * sl < T) same = same && stk[0 * CAP + spi[sl]] == g0;
                 before += __popc(m[sl]);
                 if (m[sl]) last = 32u * sl + 31 - __clz(m[sl]);
             }

@@ -469,17 +469,17 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
     // block u64 atomics when the group has too many slots (kept in registers, not in a bfs::Ctx:
     // the fallback passes one by address, which would put it in local memory)
     cnt_t *const my_cnt = s_cnt ? s_cnt + tid : nullptr;
-    auto cnt_add = [&](uint32_t slot) {
+    auto cnt_add = [&](uint32_t slot, uint32_t inc = 1u) {
         if (my_cnt) {
             cnt_t *q = my_cnt + slot * kWB;
-            uint32_t v = *q + 1u;
-            if (v >= (sizeof(cnt_t) == 4 ? 0x80000000u : 0xFFFFu)) {
+            uint32_t v = *q + inc;
+            if (v >= (sizeof(cnt_t) == 4 ? 0x80000000u : 0xFFF0u)) {
                 atomicAdd(&s_tot[slot], (unsigned long long)v);
                 v = 0;
             }
             *q = (cnt_t)v;
         } else {
-            atomicAdd(&s_tot[slot], 1ull);
+            atomicAdd(&s_tot[slot], (unsigned long long)inc);
         }
     };
     unsigned long long st[ST_N];
@@ -504,6 +504,7 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
         const uint32_t slot = gl & 0xFFFFu;
         const bool out = (s_ginfo[stk[0 * CAP + spi[0]]] & GI_KIND) == ANCHOR_OUT;
         const uint2 *ent = out ? p.out_ent : p.in_ent;
+        uint32_t nf = 0;  // completions of this lane's slots: one counter update per lane and round
 #pragma unroll
         for (int sl = 0; sl < kSlots; sl++) {
             if (lane_id + 32u * sl < T) {
@@ -513,9 +514,10 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
                 bool fresh = e.x > tp && e.x <= h;
 #pragma unroll
                 for (int k = 0; k < NV; k++) fresh = fresh && stk[(6 + k) * CAP + pi] != e.y;
-                if (fresh) cnt_add(slot);
+                nf += fresh ? 1u : 0u;
             }
         }
+        if (nf) cnt_add(slot, nf);
     };
 
     // Test the candidate entry of one slot: window entry `at` of piece `pi`.  Completions are

@@ -1156,6 +1156,7 @@ mayura_status run_enum(mayura_graph_s *g, mayura_mgtree_s *m, uint64_t rb, uint6
     cudaStream_t s = (cudaStream_t)stream;
     std::vector<DeviceTable> tabs;
     mayura_status st = ensure_tables(m, g->device, tabs);
+    if (st == MAYURA_OK) st = ensure_ranks(g);
     if (st != MAYURA_OK) return st;
     const DeviceTable &dt = tabs[0];
     const uint32_t k = m->n_motifs, ns = dt.n_slots;

@@ -119,14 +119,25 @@ __global__ void k_offsets(const uint32_t *skey, uint32_t E, uint32_t V, uint32_t
     }
 }
 
-// list entries in sorted (key, edge id) order; ids[pos] = edge id of list position pos
+// list entries in sorted (key, edge id) order; ids[pos] = edge id of list position pos, owner[pos]
+// = the list's vertex
 __global__ void k_scatter(const uint32_t *skey, const uint32_t *seid, const uint32_t *tr, const uint32_t *nbr,
-                          uint32_t E, uint2 *ent, uint32_t *ids) {
+                          uint32_t E, uint2 *ent, uint32_t *ids, uint32_t *owner) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
         const uint32_t e = seid[i];
-        const uint32_t pos = i + skey[i];
+        const uint32_t x = skey[i];
+        const uint32_t pos = i + x;
         ent[pos] = make_uint2(tr[e], nbr[e]);
         ids[pos] = e;
+        owner[pos] = x;
+    }
+}
+
+// input rank of the edge behind each list position, in place over the edge ids (enumeration only)
+__global__ void k_ranks(uint32_t *ids, const uint32_t *perm, uint32_t N) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
+        const uint32_t e = ids[p];
+        if (e != 0xFFFFFFFFu) ids[p] = perm[e];
     }
 }
 
@@ -148,13 +159,13 @@ __device__ __forceinline__ uint32_t first_after(const uint32_t *off, const uint2
 // direction -- neighbouring threads search the same list at nearby keys (cache-friendly, unlike one
 // thread per edge id).  The entry's time rank is its own list word (no gather of tr[e]); the two
 // words written land in one 16-byte eptr row.  eptr as u32 words: P(e) component k at eptr[4e + k].
-__global__ void k_succ(const uint32_t *ids, const uint2 *ent, const uint32_t *owner_of, const uint32_t *xoff,
+__global__ void k_succ(const uint32_t *ids, const uint2 *ent, const uint32_t *owner, const uint32_t *xoff,
                        const uint2 *xent, uint32_t N, uint32_t k_own, uint32_t k_cross, uint32_t *eptr) {
     for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < N; pos += gridDim.x * blockDim.x) {
         const uint32_t e = ids[pos];
         if (e == 0xFFFFFFFFu) continue;  // a sentinel position
         const uint32_t key = ent[pos].x;
-        const uint32_t x = owner_of[e];
+        const uint32_t x = owner[pos];
         uint32_t q = pos + 1;
         while (ent[q].x <= key) ++q;  // ties; the list's sentinel (time rank 0xFFFFFFFF) stops it
         eptr[4 * (size_t)e + k_own] = q;
@@ -162,12 +173,10 @@ __global__ void k_succ(const uint32_t *ids, const uint2 *ent, const uint32_t *ow
     }
 }
 
-__global__ void k_entry_ptr(const uint32_t *ids, const uint4 *eptr, const uint32_t *perm, uint32_t N, uint4 *ptr,
-                            uint32_t *rank) {
+__global__ void k_entry_ptr(const uint32_t *ids, const uint4 *eptr, uint32_t N, uint4 *ptr) {
     for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
         const uint32_t e = ids[p];
         ptr[p] = e != 0xFFFFFFFFu ? eptr[e] : make_uint4(0, 0, 0, 0);
-        rank[p] = e != 0xFFFFFFFFu ? perm[e] : 0xFFFFFFFFu;
     }
 }
 
@@ -383,7 +392,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     g->device_bytes += bytes;
 
     Tmp tmp;
-    uint32_t *isrc, *idst, *bad, *val, *val2, *skey, *ids[2];
+    uint32_t *isrc, *idst, *bad, *val, *val2, *skey, *owner[2];
     int64_t *it;
     uint64_t *key, *key2;
     GK(tmp.get(isrc, E), "cudaMalloc(tmp)");
@@ -459,15 +468,18 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     // 3. out / in adjacency
     GK(tmp.get(skey, E), "cudaMalloc(tmp)");
     GK(tmp.get(val2, E), "cudaMalloc(tmp)");
-    GK(tmp.get(ids[0], N + 1), "cudaMalloc(tmp)");
-    GK(tmp.get(ids[1], N + 1), "cudaMalloc(tmp)");
+    GK(tmp.get(owner[0], N + 1), "cudaMalloc(tmp)");
+    GK(tmp.get(owner[1], N + 1), "cudaMalloc(tmp)");
+    // the edge id behind each list position goes into the rank arrays (filled with 0xFF: sentinel
+    // positions stay 0xFFFFFFFF); the first enumeration turns them into input ranks (ensure_ranks)
+    uint32_t *ids[2] = {g->d_out_rank, g->d_in_rank};
+    g->ranks_ready = false;
     const int vbits = std::max(1, bits_for(V ? V - 1 : 0));
     for (int dir = 0; dir < 2; dir++) {
         const uint32_t *k_in = dir == 0 ? g->d_src : g->d_dst;
         const uint32_t *nbr = dir == 0 ? g->d_dst : g->d_src;
         uint32_t *off = dir == 0 ? g->d_out_off : g->d_in_off;
         uint2 *ent = reinterpret_cast<uint2 *>(dir == 0 ? g->d_out_ent : g->d_in_ent);
-        GK(cudaMemsetAsync(ids[dir], 0xFF, 4 * (N + 1), s), "memset(ids)");
         if (E) {
             k_iota<<<blocks_for(E), kT, 0, s>>>(val, E); count_launch();
             size_t need = 0;
@@ -476,7 +488,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
             GK(tmp.get(ct, need), "cudaMalloc(tmp)");
             GK(cub::DeviceRadixSort::SortPairs(ct, need, k_in, skey, val, val2, (int)E, 0, vbits, s), "cub sort");
             trace("load: vertex sort");
-            k_scatter<<<blocks_for(E), kT, 0, s>>>(skey, val2, g->d_tr, nbr, E, ent, ids[dir]); count_launch();
+            k_scatter<<<blocks_for(E), kT, 0, s>>>(skey, val2, g->d_tr, nbr, E, ent, ids[dir], owner[dir]); count_launch();
         }
         k_offsets<<<blocks_for((uint64_t)V + 1), kT, 0, s>>>(skey, E, V, off); count_launch();
     }
@@ -484,20 +496,20 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     // 4. successor pointers, then each list entry's copy of them
     if (E) {
         // out-list positions: components 0 (own) and 3 (in(src)); in-list positions: 1 (own), 2 (out(dst))
-        k_succ<<<blocks_for(N), kT, 0, s>>>(ids[0], reinterpret_cast<const uint2 *>(g->d_out_ent), g->d_src, g->d_in_off,
+        k_succ<<<blocks_for(N), kT, 0, s>>>(ids[0], reinterpret_cast<const uint2 *>(g->d_out_ent), owner[0], g->d_in_off,
                                             reinterpret_cast<const uint2 *>(g->d_in_ent), (uint32_t)N, 0u, 3u, g->d_eptr);
         count_launch();
-        k_succ<<<blocks_for(N), kT, 0, s>>>(ids[1], reinterpret_cast<const uint2 *>(g->d_in_ent), g->d_dst, g->d_out_off,
+        k_succ<<<blocks_for(N), kT, 0, s>>>(ids[1], reinterpret_cast<const uint2 *>(g->d_in_ent), owner[1], g->d_out_off,
                                             reinterpret_cast<const uint2 *>(g->d_out_ent), (uint32_t)N, 1u, 2u, g->d_eptr);
         count_launch();
         trace("load: successor pointers (by edge)");
     }
     if (N) {
-        k_entry_ptr<<<blocks_for(N), kT, 0, s>>>(ids[0], reinterpret_cast<const uint4 *>(g->d_eptr), g->d_perm,
-                                                 (uint32_t)N, reinterpret_cast<uint4 *>(g->d_out_ptr), g->d_out_rank);
+        k_entry_ptr<<<blocks_for(N), kT, 0, s>>>(ids[0], reinterpret_cast<const uint4 *>(g->d_eptr), (uint32_t)N,
+                                                 reinterpret_cast<uint4 *>(g->d_out_ptr));
         count_launch();
-        k_entry_ptr<<<blocks_for(N), kT, 0, s>>>(ids[1], reinterpret_cast<const uint4 *>(g->d_eptr), g->d_perm,
-                                                 (uint32_t)N, reinterpret_cast<uint4 *>(g->d_in_ptr), g->d_in_rank);
+        k_entry_ptr<<<blocks_for(N), kT, 0, s>>>(ids[1], reinterpret_cast<const uint4 *>(g->d_eptr), (uint32_t)N,
+                                                 reinterpret_cast<uint4 *>(g->d_in_ptr));
         count_launch();
     }
     GK(cudaGetLastError(), "graph build kernels");
@@ -556,6 +568,22 @@ mayura_status copy_t_host(mayura_graph_s *g, std::vector<int64_t> &t) {
     const cudaError_t e = g->E ? cudaMemcpy(t.data(), g->d_t, 8 * g->E, cudaMemcpyDeviceToHost) : cudaSuccess;
     cudaSetDevice(prev);
     if (e != cudaSuccess) return fail(MAYURA_E_CUDA, std::string("copy_t_host: ") + cudaGetErrorString(e));
+    return MAYURA_OK;
+}
+
+// The enumeration's input ranks per list position, converted in place from the edge ids the build
+// left there (once per graph; the counting path never reads them).
+mayura_status ensure_ranks(mayura_graph_s *g) {
+    if (g->ranks_ready || g->device < 0) return MAYURA_OK;
+    const size_t N = (size_t)g->E + g->V;
+    if (N) {
+        k_ranks<<<blocks_for(N), kT>>>(g->d_out_rank, g->d_perm, (uint32_t)N);
+        k_ranks<<<blocks_for(N), kT>>>(g->d_in_rank, g->d_perm, (uint32_t)N);
+        count_launch(2);
+    }
+    GK(cudaGetLastError(), "rank kernels");
+    GK(cudaStreamSynchronize(0), "ranks");
+    g->ranks_ready = true;
     return MAYURA_OK;
 }
 

@@ -88,6 +88,7 @@ struct mayura_graph_s {
     uint32_t *d_perm = nullptr;                           // input rank of edge id (GPU-built graphs)
     char *d_arena = nullptr;                              // the one allocation holding the arrays above
     uint32_t *d_out_rank = nullptr, *d_in_rank = nullptr; // input rank of the edge behind each list position
+    bool ranks_ready = false;  // d_*_rank hold edge ids until the first enumeration converts them (ensure_ranks)
     uint32_t *d_enum = nullptr;                           // enumeration scratch (per-warp counts / bases)
     size_t enum_bytes = 0;
     uint32_t *d_queue = nullptr;                         // work-queue cursors
@@ -133,6 +134,7 @@ constexpr size_t kPadE = 32, kPadEnt = 64;
 mayura_status build_graph_device(const uint32_t *src, const uint32_t *dst, const int64_t *t, uint64_t E,
                                  uint32_t V, mayura_graph_s *g);
 mayura_status ensure_host(mayura_graph_s *g);
+mayura_status ensure_ranks(mayura_graph_s *g);
 mayura_status copy_t_host(mayura_graph_s *g, std::vector<int64_t> &t);
 // device path of mayura_partition_roots: cut[p] (1 <= p < n_parts) = first root index whose
 // proxy prefix reaches floor(total * p / n_parts) (capi.cpp documents the proxy)

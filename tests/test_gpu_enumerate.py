@@ -150,3 +150,24 @@ def test_enum_form_reports_the_form_that_ran(M, request):
     assert M.mayura_enum_form(g.handle) == want
     g.close()
     tree.close()
+
+
+def test_enumerate_repeated_on_one_graph(M, oracle_mod):
+    """The input ranks behind list positions are computed on the first enumeration of a graph
+    (in place over the edge ids the build leaves there); later enumerations of the same graph,
+    with other groups and root ranges, and counting in between, must read the same ranks."""
+    src, dst, t, V = synth.random_graph(41, 30, 3_000, 900, 0.02)
+    g = M.Graph(src, dst, t, V, device=0)
+    groups = [synth.group(synth.GROUP_C2), [[(0, 1), (1, 2)], [(0, 1), (1, 0)]], synth.group(synth.GROUP_C2)]
+    E = len(src)
+    for i, motifs in enumerate(groups):
+        tree = M.MGTree(motifs, 25)
+        rr = None if i != 1 else (E // 4, E // 2)
+        M.comine(g, tree)
+        counts, lists = M.enumerate_matches(g, tree, rr)
+        assert counts == M.comine(g, tree, rr)
+        for q, mo in enumerate(motifs):
+            exp = oracle_mod.enumerate_matches(src, dst, t, V, mo, 25, rr)
+            assert np.array_equal(_sorted_rows(lists[q]), _sorted_rows(exp)), (i, q)
+        tree.close()
+    g.close()

@@ -402,12 +402,11 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     uint64_t *sd;
     GK(tmp.get(sd, E), "cudaMalloc(tmp)");
     trace("load: allocations");
-    // t is copied first; src/dst follow on a side stream while t is reduced and sorted on the main
-    // one: the sort by time needs only t, so it overlaps the second half of the H2D traffic (the
-    // side copies wait for t's: issued together they would share the link and t would land last)
+    // src/dst travel on a side stream while t is copied, reduced and sorted on the main one:
+    // the sort by time needs only t, so the second half of the H2D traffic overlaps it
+    // (issuing t's copy first and holding the side copies behind it measured the same e2e, w54)
     SideStream &ss = side_stream(g->device);
     std::unique_lock<std::mutex> side_lock(ss.mu);  // one build at a time uses this device's side stream
-    GK(cudaMemcpyAsync(it, ht, 8ull * E, cudaMemcpyHostToDevice, s), "H2D(t)");
     GK(cudaEventRecord(ss.ev0, s), "event");
     GK(cudaStreamWaitEvent(ss.s2, ss.ev0, 0), "stream wait");
     GK(cudaMemsetAsync(bad, 0, 16, ss.s2), "memset");
@@ -419,6 +418,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     }
     GK(cudaMemcpyAsync(ss.hbad, bad, 4, cudaMemcpyDeviceToHost, ss.s2), "D2H(check)");
     GK(cudaEventRecord(ss.ev2, ss.s2), "event");
+    GK(cudaMemcpyAsync(it, ht, 8ull * E, cudaMemcpyHostToDevice, s), "H2D(t)");
     // time range -> key bits
     int64_t *mm;
     GK(tmp.get(mm, 2), "cudaMalloc(tmp)");

@@ -83,8 +83,11 @@ __global__ void k_gather(const uint32_t *perm, const uint64_t *sd, const uint64_
 }
 
 // tr[i] = first index with t == t[i] (t sorted): a backward step over the (rare) ties, a
-// bisection when the tie run is long
-__global__ void k_time_rank(const int64_t *t, uint32_t *tr, uint32_t E) {
+// bisection when the tie run is long.  The list entries {tr, neighbour} of edge i are written
+// beside it (out-lists: {tr, dst}, in-lists: {tr, src}), so the scatter into the lists gathers one
+// 8-byte word per edge
+__global__ void k_time_rank(const int64_t *t, const uint32_t *src, const uint32_t *dst, uint32_t *tr, uint2 *ent_out,
+                            uint2 *ent_in, uint32_t E) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
         const int64_t x = t[i];
         uint32_t j = i;
@@ -99,6 +102,8 @@ __global__ void k_time_rank(const int64_t *t, uint32_t *tr, uint32_t E) {
             j = lo;
         }
         tr[i] = j;
+        ent_out[i] = make_uint2(j, dst[i]);
+        ent_in[i] = make_uint2(j, src[i]);
     }
 }
 
@@ -121,13 +126,13 @@ __global__ void k_offsets(const uint32_t *skey, uint32_t E, uint32_t V, uint32_t
 
 // list entries in sorted (key, edge id) order; ids[pos] = edge id of list position pos, owner[pos]
 // = the list's vertex
-__global__ void k_scatter(const uint32_t *skey, const uint32_t *seid, const uint32_t *tr, const uint32_t *nbr,
-                          uint32_t E, uint2 *ent, uint32_t *ids, uint32_t *owner) {
+__global__ void k_scatter(const uint32_t *skey, const uint32_t *seid, const uint2 *ent_of, uint32_t E, uint2 *ent,
+                          uint32_t *ids, uint32_t *owner) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
         const uint32_t e = seid[i];
         const uint32_t x = skey[i];
         const uint32_t pos = i + x;
-        ent[pos] = make_uint2(tr[e], nbr[e]);
+        ent[pos] = ent_of[e];
         ids[pos] = e;
         owner[pos] = x;
     }
@@ -463,7 +468,9 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
         k_gather<<<blocks_for(E), kT, 0, s>>>(g->d_perm, sd, key2, tmin, g->d_src, g->d_dst, g->d_t, E); count_launch();
         trace("load: gather");
         // 2. time ranks
-        k_time_rank<<<blocks_for(E), kT, 0, s>>>(g->d_t, g->d_tr, E); count_launch();
+        // the list-entry words per edge reuse the sort's input keys and the packed endpoints (both consumed)
+        k_time_rank<<<blocks_for(E), kT, 0, s>>>(g->d_t, g->d_src, g->d_dst, g->d_tr, reinterpret_cast<uint2 *>(key),
+                                                 reinterpret_cast<uint2 *>(sd), E); count_launch();
     }
     trace("load: time sort + ranks");
     // 3. out / in adjacency
@@ -478,7 +485,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
     const int vbits = std::max(1, bits_for(V ? V - 1 : 0));
     for (int dir = 0; dir < 2; dir++) {
         const uint32_t *k_in = dir == 0 ? g->d_src : g->d_dst;
-        const uint32_t *nbr = dir == 0 ? g->d_dst : g->d_src;
+        const uint2 *ent_of = reinterpret_cast<const uint2 *>(dir == 0 ? key : sd);
         uint32_t *off = dir == 0 ? g->d_out_off : g->d_in_off;
         uint2 *ent = reinterpret_cast<uint2 *>(dir == 0 ? g->d_out_ent : g->d_in_ent);
         if (E) {
@@ -489,7 +496,7 @@ mayura_status build_graph_device(const uint32_t *hsrc, const uint32_t *hdst, con
             GK(tmp.get(ct, need), "cudaMalloc(tmp)");
             GK(cub::DeviceRadixSort::SortPairs(ct, need, k_in, skey, val, val2, (int)E, 0, vbits, s), "cub sort");
             trace("load: vertex sort");
-            k_scatter<<<blocks_for(E), kT, 0, s>>>(skey, val2, g->d_tr, nbr, E, ent, ids[dir], owner[dir]); count_launch();
+            k_scatter<<<blocks_for(E), kT, 0, s>>>(skey, val2, ent_of, E, ent, ids[dir], owner[dir]); count_launch();
         }
         k_offsets<<<blocks_for((uint64_t)V + 1), kT, 0, s>>>(skey, E, V, off); count_launch();
     }

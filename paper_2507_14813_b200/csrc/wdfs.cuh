@@ -771,12 +771,12 @@ __global__ void __launch_bounds__(kWB, WDFS_MINB) wdfs_kernel(const __grid_const
         for (int sl = 0; sl < kSlots; sl++) {
             if (sl >= 1) {
                 has = (hmask >> sl) & 1u;
-                if (!__any_sync(kFull, has)) continue;
-                if (has) stage_get<MAXV>(sg + (sl - 1) * Stage<MAXV>::F * 32, lane_id, x, c_lo, c_end, c_out, s_nodes);
             }
-            if (__any_sync(kFull, has))
-                open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, has, x, c_lo, c_end, c_out,
-                                                 my_cnt, s_tot, st);
+            if (!__any_sync(kFull, has)) continue;
+            if (sl >= 1 && has)
+                stage_get<MAXV>(sg + (sl - 1) * Stage<MAXV>::F * 32, lane_id, x, c_lo, c_end, c_out, s_nodes);
+            open_push<MAXV, GEN, CAP, STATS>(w, s_nodes, s_groups, stk, ps, sp, sp_top, has, x, c_lo, c_end, c_out,
+                                             my_cnt, s_tot, st);
         }
     }
 
